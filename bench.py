@@ -1,0 +1,395 @@
+"""Benchmark: grid-point updates per second of the fused stencil path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c2|c3|c1]
+                    [--impl ours|reference]
+
+Workload (default c4 = BASELINE.json configs[3], the config the north-star
+"GLUP/s at 1/2/4/8 B200" metric and its >=80 %-of-HBM target are quoted on):
+3-D 7-point Jacobi on a 1024^3 float64 grid, unit Dirichlet faces. One STEP is
+one batch of 100 Jacobi iterations (the reference client's default flush
+depth, pkg/src/elastencil/client.py:168) submitted as DAG bytes through the
+worker seam and executed by the generated sm_100a kernels. Arrays (2 x 8.6 GB)
+are far larger than L2 (126 MB), so no L2 flush is needed between steps.
+
+`value`  : device time (CUDA events on the compute stream), max over ranks.
+`e2e`    : host wall clock through the public API per step (DAG bytes in,
+           one result plane fetched to host), max over ranks.
+`roofline`: the node kernel, achieved = algorithmic bytes per launch / mean
+           CUDA-event kernel duration, against MEASURED_PEAKS.json hbm_gbs.
+`cpu_baseline`: the strict-order C oracle (oracle/strict_eval.c) on all host
+           cores over a bounded z-slab sample of the same grid (rank 0, N=1).
+--impl reference: the reference's CPU path restated (the oracle port) timed on
+           the host cores over that bounded sample per step (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOADS = {
+    "c4": dict(kind="heat3d", n=1024, iters_per_step=100, dtype="f64",
+               label="C4: 3-D 7-point Jacobi 1024^3 fp64 (BASELINE configs[3])"),
+    "c2": dict(kind="heat3d", n=512, iters_per_step=100, dtype="f64",
+               label="C2: 3-D 7-point heat 512^3 fp64 (BASELINE configs[1])"),
+    "c3": dict(kind="wave2d", n=16384, iters_per_step=100, dtype="f32",
+               label="C3: 2-D acoustic wave r=2 16384^2 fp32 (BASELINE configs[2])"),
+    "c1": dict(kind="laplace", n=1024, iters_per_step=100, dtype="f64",
+               label="C1: 2-D 5-point Jacobi 1024^2 fp64 (BASELINE configs[0])"),
+}
+METRIC = "GLUP/s (grid-point updates/s)"
+
+
+def lup_per_iter(w) -> int:
+    n = w["n"]
+    if w["kind"] == "heat3d":
+        return (n - 2) ** 3
+    if w["kind"] == "wave2d":
+        return (n - 4) ** 2
+    return (n - 2) ** 2
+
+
+def bytes_per_iter(w) -> int:
+    """Algorithmic HBM bytes of one iteration."""
+    n = w["n"]
+    if w["kind"] == "heat3d":
+        m = n - 2
+        return 8 * (m ** 3 + 6 * m ** 2 + m ** 3)
+    if w["kind"] == "wave2d":
+        m = n - 4
+        return 4 * ((m * m + 8 * m) + m * m + m * m)
+    m = n - 2
+    return 8 * (m * m + 4 * m + m * m)
+
+
+def load_peaks() -> tuple:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        p = json.load(open(path))
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle port, test infrastructure)
+
+def cpu_sample(w, iters: int = 2, planes: int = 34, threads: int = 0) -> dict:
+    """Strict-order C oracle on a bounded sample of the workload, all host cores."""
+    from oracle.oracle import _lib as olib, strict_eval_statement
+    from paper_2512_19851_b200.analysis import compile_plan
+    from paper_2512_19851_b200.programs import DagProgram, heat3d_program, laplace_program, wave2d_program
+    from paper_2512_19851_b200.wire import DTYPE_F32
+
+    n = w["n"]
+    prog = DagProgram()
+    if w["kind"] == "heat3d":
+        shape = (planes, n, n)
+        heat3d_program(prog, n, 1, shape=shape)
+        sample = f"{iters} Jacobi iterations over a {planes}x{n}x{n} z-slab of the {n}^3 grid"
+    elif w["kind"] == "wave2d":
+        rows = max(planes * 16, 64)
+        shape = (rows, n)
+        from paper_2512_19851_b200.programs import wave2d_tree
+        u = [prog.create_array(shape, DTYPE_F32) for _ in range(3)]
+        prog.assign(u[2], (slice(2, -2), slice(2, -2)), wave2d_tree(u[0], u[1]))
+        sample = f"{iters} wave steps over a {rows}x{n} row-slab of the {n}^2 grid"
+    else:
+        shape = (n, n)
+        laplace_program(prog, n, 1)
+        sample = f"{iters} Jacobi iterations over the full {n}^2 grid"
+    node = prog.dag.nodes[-1]
+    plan = compile_plan(node, prog.dag.ast_table).statements[0]
+    dt = np.float32 if w["dtype"] == "f32" else np.float64
+    rng = np.random.default_rng(0)
+    arrays = {a: rng.random(shape).astype(dt) for a in prog.shapes}
+    strict_eval_statement(plan, arrays, threads)  # warm (page faults, thread pool)
+    cores = threads or olib().oracle_max_threads()
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        strict_eval_statement(plan, arrays, threads)
+    dt_s = time.perf_counter() - t0
+    lups = int(np.prod([b - a for a, b in plan.output_slice_bounds])) * iters
+    return {"value": lups / dt_s / 1e9, "unit": "GLUP/s", "cores": int(cores), "kind": "port",
+            "sample": sample + " (oracle/strict_eval.c, -ffp-contract=off, OpenMP)",
+            "seconds": dt_s}
+
+
+def run_reference_arm(args, w):
+    """The reference's CPU path (oracle port) on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    planes = 34 if w["kind"] == "heat3d" else 8
+    for _ in range(args.warmup):
+        cpu_sample(w, iters=1, planes=planes)
+    vals = []
+    t0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_sample(w, iters=1, planes=planes)
+        vals.append(last["value"])
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GLUP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic",
+        "config": {"workload": w["label"], "grid": [w["n"]] * (3 if w["kind"] == "heat3d" else 2)},
+        "cpu_baseline": {"value": value, "unit": "GLUP/s", "cores": last["cores"], "kind": "port",
+                         "sample": "each step: " + last["sample"]},
+        "e2e": {"value": value, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+
+def build_job(w, world: int, rank: int, skeleton: str = "auto"):
+    from paper_2512_19851_b200.programs import DagProgram, heat3d_setup, laplace_program, wave2d_setup
+    from paper_2512_19851_b200.session import GpuJob
+    from paper_2512_19851_b200.wire import DTYPE_F32, DTYPE_F64
+
+    if world > 1:
+        from paper_2512_19851_b200.ipc import IpcGpuJob
+
+        job = IpcGpuJob(rank, world, device=int(os.environ.get("LOCAL_RANK", rank)),
+                        skeleton=skeleton)
+    else:
+        job = GpuJob(workers=1, skeleton=skeleton)
+    prog = DagProgram()
+    n = w["n"]
+    if w["kind"] == "heat3d":
+        arrays = heat3d_setup(prog, n)
+    elif w["kind"] == "wave2d":
+        arrays = wave2d_setup(prog, n, DTYPE_F32)
+    else:
+        laplace_program(prog, n, 0)
+        arrays = (0, 1)
+    for aid in sorted(prog.shapes):
+        job.create_array(prog.shapes[aid], prog.dtypes.get(aid, DTYPE_F64))
+    job.run(prog.dag)
+    job.sync()
+    return job, prog, arrays
+
+
+def step_dag(w, prog_shapes, dtypes, arrays):
+    """DAG bytes of one step (iters_per_step iterations; roles return to start)."""
+    from paper_2512_19851_b200.programs import DagProgram, heat3d_iterations, laplace_iteration_statements, wave2d_steps
+    from paper_2512_19851_b200.wire import encode_dag
+
+    prog = DagProgram()
+    for aid in sorted(prog_shapes):
+        prog.builder.declare_array(aid, prog_shapes[aid])
+    k = w["iters_per_step"]
+    if w["kind"] == "heat3d":
+        heat3d_iterations(prog, arrays[0], arrays[1], k)
+    elif w["kind"] == "wave2d":
+        wave2d_steps(prog, *arrays, k)
+    else:
+        laplace_iteration_statements(prog, arrays[0], arrays[1], k)
+    return encode_dag(prog.dag)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skeleton", default="auto", choices=["auto", "point", "stream"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, w)
+        return
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # plumbing only: barrier + max-over-ranks
+        dist.init_process_group("gloo")
+    from paper_2512_19851_b200.wire import decode_dag
+
+    job, prog, arrays = build_job(w, world, rank, args.skeleton)
+    blob = step_dag(w, prog.shapes, prog.dtypes, arrays)
+    ex = job.executors[0]
+    dev = job.devs[0]
+
+    def one_step():
+        return job.run(decode_dag(blob))
+
+    for _ in range(args.warmup):
+        one_step()
+    job.sync()
+
+    # ---- device-timed region ------------------------------------------------
+    if dist:
+        dist.barrier()
+    job.sync()
+    clocks = ClockSampler(dev.index).start()
+    ev0, ev1 = dev.event(), dev.event()
+    ex.time_kernels = True
+    ex.kernel_events.clear()
+    launches0 = dev.launches
+    ev0.record()
+    for _ in range(args.steps):
+        one_step()
+    ev1.record()
+    ev1.sync()
+    job.sync()
+    clock = clocks.stop()
+    gpu_launches = dev.launches - launches0
+    dev_ms = ev0.elapsed_ms(ev1)
+    kt = [a.elapsed_ms(b) for a, b in ex.kernel_events]
+    ex.time_kernels = False
+    for a, b in ex.kernel_events:
+        a.close(), b.close()
+    ex.kernel_events.clear()
+    if dist:
+        import torch
+        t = torch.tensor([dev_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+
+    lups_step = lup_per_iter(w) * w["iters_per_step"]
+    value = lups_step * args.steps / (dev_ms / 1e3) / 1e9
+
+    # ---- end-to-end through the public API ------------------------------------
+    from paper_2512_19851_b200.device import PinnedBuffer
+    plane_bounds = None
+    shape = prog.shapes[arrays[0]]
+    mid = shape[0] // 2
+    plane_bounds = ((mid, mid + 1),) + tuple((0, e) for e in shape[1:])
+    d2h = int(np.prod([b - a for a, b in plane_bounds])) * (4 if w["dtype"] == "f32" else 8)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one_step()
+        job.fetch_local(arrays[0], plane_bounds) if hasattr(job, "fetch_local") else job.fetch(arrays[0], plane_bounds)
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        import torch
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = lups_step * args.steps / e2e_s / 1e9
+
+    # ---- roofline ------------------------------------------------------------
+    peak, peak_src = load_peaks()
+    mean_k = statistics.mean(kt) if kt else dev_ms / max(1, args.steps * w["iters_per_step"])
+    bytes_launch = bytes_per_iter(w) // world if world > 1 else bytes_per_iter(w)
+    achieved = bytes_launch / (mean_k / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(args.workload, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GLUP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic",
+        "config": {"workload": w["label"], "grid": list(shape),
+                   "iterations_per_step": w["iters_per_step"],
+                   "parallelism": f"slabs over {world} GPU(s)" if world > 1 else "1 GPU, 1 tile",
+                   "l2": "inputs larger than L2 (2 arrays x %.1f GB), no flush" % (
+                       np.prod(shape) * (4 if w["dtype"] == "f32" else 8) / 1e9),
+                   "skeleton": args.skeleton},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel_ms": mean_k, "bytes_per_launch": bytes_launch,
+                     "peak_source": peak_src,
+                     "frac_of_8TBs": achieved / 8000.0},
+        "e2e": {"value": e2e_val, "unit": "GLUP/s",
+                "h2d_bytes_per_step": len(blob), "d2h_bytes_per_step": d2h,
+                "note": "host DAG bytes -> decode/analyze/codegen-cache -> launches; one result plane fetched"},
+        "gpu_launches": gpu_launches,
+        "clocks": clock,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample(w)
+        line["cpu_baseline"].pop("seconds", None)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    job.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

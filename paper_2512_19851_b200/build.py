@@ -1,0 +1,90 @@
+"""Build recipe: libest.so (nvcc, sm_100a), the oracle's C evaluator, and an
+offline NVRTC prebuild of the kernels the bench / smoke / tests instantiate
+(so a fresh GPU box loads cubins from the in-tree cache instead of compiling).
+Runs without a GPU."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+HOST_CC = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+
+
+def build_libest(verbose: bool = False) -> str:
+    src = os.path.join(HERE, "csrc", "est.cu")
+    out = os.path.join(HERE, "libest.so")
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+           "-ccbin", HOST_CC, "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
+           "-I", os.path.join(ROOT, "include"), "-o", out, src, "-lnvrtc",
+           "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+    return out
+
+
+def build_oracle() -> str:
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+    return os.path.join(ROOT, "oracle", "liboracle.so")
+
+
+def precompile_sources(sources) -> tuple:
+    """NVRTC-compile kernel sources into the in-tree cache (no GPU needed)."""
+    from . import _lib
+    from .device import DEFAULT_CACHE, NVRTC_OPTS
+
+    lib = _lib.load()
+    opts = (C.c_char_p * len(NVRTC_OPTS))(*[o.encode() for o in NVRTC_OPTS])
+    new = cached = 0
+    for src in sources:
+        was = C.c_int(0)
+        _lib.check(lib.est_module_precompile(src.encode(), opts, len(NVRTC_OPTS),
+                                             DEFAULT_CACHE.encode(), C.byref(was)))
+        cached += was.value
+        new += 1 - was.value
+    return new, cached
+
+
+def standard_sources() -> list:
+    """Kernel sources for the bench workloads, smoke and the parity suites."""
+    from .analysis import compile_plan
+    from .codegen import kernel_source_for
+    from .ir import fuse
+    from .programs import (DagProgram, cavity_program, heat3d_program, laplace_program,
+                           wave2d_program)
+    from .wire import DTYPE_F32
+
+    progs = []
+    p = DagProgram(); laplace_program(p, 64, 2); progs.append(p)
+    p = DagProgram(); heat3d_program(p, 16, 2, seed_fills=2); progs.append(p)
+    p = DagProgram(); wave2d_program(p, 64, 2, dtype=DTYPE_F32); progs.append(p)
+    p = DagProgram(); cavity_program(p, 16, 1, pressure_iters=1); progs.append(p)
+    srcs = set()
+    for p in progs:
+        for dag in (p.dag, fuse(p.dag)):
+            for node in dag.nodes:
+                out = node.statements[0].output
+                rank, dt = len(p.shapes[out]), p.dtypes.get(out, 0)
+                plan = compile_plan(node, dag.ast_table)
+                for skel in ("auto", "point"):
+                    srcs.add(kernel_source_for(plan, rank, dt, skel)[0])
+    return sorted(srcs)
+
+
+def build_all(prebuild: bool = True) -> None:
+    build_libest()
+    build_oracle()
+    if prebuild:
+        new, cached = precompile_sources(standard_sources())
+        print(f"[build] kernel cache: {new} compiled, {cached} already cached", file=sys.stderr)
+
+
+if __name__ == "__main__":
+    build_all()

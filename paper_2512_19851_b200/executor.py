@@ -1,0 +1,238 @@
+"""GpuExecutor: one worker's DAG-batch execution on its GPU.
+
+Drop-in for pkg/src/elastencil/executor.py:179-348 (`Executor(store,
+exchanges).execute_batch(dag) -> BatchStats`, persistent `depths`):
+
+* prepare_batch — identical host logic: analyze, compile plans, monotone ghost
+  depth growth (device realloc, local-epoch bump on growth), and the push plan
+  that starts each halo round right after the array's last writer
+  (executor.py:193-256). Errors are raised here before any launch.
+* execution — nodes are issued in node-id order (a topological order of the
+  DAG, and the order the reference's ready-heap yields when nothing waits) as
+  stream-ordered device work: one generated kernel launch per node covering
+  every owned tile and every fused statement (work items of one grid), the
+  halo rounds as batched device copies / peer pulls at exactly the points the
+  reference starts them. The host never waits on the device inside a batch;
+  the worker synchronises only before answering FETCH/MIGRATE/CHECKPOINT/EXIT
+  (SURVEY.md §8b pipelining note).
+
+Stats keep the reference definitions (kernel_launches = one per node per owned
+tile, rounds per array, net_messages); `gpu_launches` counts the device
+kernels actually launched and `device_ms` is CUDA-event time when requested.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+from . import codegen
+from .analysis import analyze_dag, compile_plan
+from .device import COMPUTE
+from .errors import MalformedDag
+
+
+@dataclass
+class BatchStats:
+    nodes_executed: int = 0
+    kernel_launches: int = 0
+    rounds: dict = field(default_factory=dict)
+    net_messages: int = 0
+    wall_ms: float = 0.0
+    node_ms: dict = field(default_factory=dict)
+    compute_ms: float = 0.0
+    wait_ms: float = 0.0
+    prepare_ms: float = 0.0
+    gpu_launches: int = 0
+    device_ms: float | None = None
+
+
+def node_hazard(node) -> bool:
+    """True if a node's statements depend on each other (reads/writes overlap).
+
+    fuse() never builds such nodes (ir.py:519-526), but validate_dag accepts
+    them and the reference then diverges from its own oracle on multi-tile runs
+    (SURVEY.md §8a "Hazard"). The backend rejects them (MalformedDag).
+    """
+    written: set = set()
+    read: set = set()
+    for st in node.statements:
+        if st.output in written or st.output in read or written & set(st.inputs):
+            return True
+        written.add(st.output)
+        read.update(st.inputs)
+    return False
+
+
+class GpuExecutor:
+    def __init__(self, store, exchanges, skeleton: str = "auto"):
+        self.store = store
+        self.exchanges = exchanges
+        self.dev = store.dev
+        self.depths: dict = {}
+        self.idle_wait = None        # kept for API parity (executor.py:186-189)
+        self.skeleton = skeleton     # "auto" | "point" | "stream"
+        self._plan_cache: dict = {}
+        self.time_kernels = False    # bracket every node kernel with events
+        self.transport = None        # peer transport when the job has >1 worker
+        self.kernel_events: list = []
+
+    # -- preparation (executor.py:193-256) ----------------------------------
+    def prepare_batch(self, dag):
+        shapes = {a: info.shape for a, info in self.store.arrays.items()}
+        metas = analyze_dag(dag, shapes)
+        plans = [compile_plan(n, dag.ast_table) for n in dag.nodes]
+        for node in dag.nodes:
+            if len(node.statements) > 1 and node_hazard(node):
+                raise MalformedDag(f"node {node.node_id} has dependent statements")
+            dts = {self.store.arrays[a].dtype for s in node.statements for a in (s.output, *s.inputs)}
+            if len(dts) > 1:
+                raise MalformedDag(f"node {node.node_id} mixes element types")
+        need: dict = {}
+        for m in metas:
+            for a, off in m.array_max_offset.items():
+                need[a] = off if a not in need else tuple(map(max, need[a], off))
+        changed = False
+        for a, off in sorted(need.items()):
+            old = self.depths.get(a, (0,) * len(off))
+            new = tuple(map(max, old, off))
+            self.store.check_depth_fits(a, new)
+            self.depths[a] = new
+            changed |= new != old
+        # depth changes are identical on every worker (pure in the DAG), so all
+        # workers - owning tiles or not - meet in the same realloc barriers
+        if changed and self.transport is not None:
+            self.transport.before_realloc()
+        for a in sorted(need):
+            if self.store.ensure_ghost_capacity(a, self.depths[a]):
+                self.store.bump_local_epoch(a)
+        if changed and self.transport is not None:
+            self.transport.after_realloc()
+        local: dict = {}
+        ghost: dict = {}
+        last_writer: dict = {}
+        pushes: dict = {}
+        for node, meta in zip(dag.nodes, metas):
+            for a in sorted(meta.array_max_offset):
+                if not meta.needs_exchange(a):
+                    continue
+                target = local.setdefault(a, self.store.local_epoch(a))
+                current = ghost.setdefault(a, self.exchanges.ghost_generation(a))
+                if target == 0 or current == target:
+                    continue
+                pushes.setdefault(last_writer.get(a), []).append((a, target))
+                ghost[a] = target
+            for a in node.writes:
+                local[a] = local.get(a, self.store.local_epoch(a)) + 1
+                last_writer[a] = node.node_id
+        return metas, plans, pushes
+
+    # -- execution (executor.py:258-348) ------------------------------------
+    def execute_batch(self, dag) -> BatchStats:
+        t0 = time.perf_counter()
+        before = self.exchanges.snapshot_stats()
+        launches0 = self.dev.launches
+        metas, plans, pushes = self.prepare_batch(dag)
+        stats = BatchStats(prepare_ms=(time.perf_counter() - t0) * 1e3)
+        for a, e in pushes.get(None, ()):
+            self.exchanges.ensure_round(a, e)
+        for node in dag.nodes:
+            meta = metas[node.node_id]
+            for a in sorted(meta.array_max_offset):
+                if not meta.needs_exchange(a):
+                    continue
+                target = self.store.local_epoch(a)
+                if target and self.exchanges.ghost_generation(a) != target:
+                    self.exchanges.ensure_round(a, target)
+            t_node = time.perf_counter()
+            if self.transport is not None:
+                for a in sorted(node.writes):
+                    self.transport.before_write(a)
+            self.launch_node(node, plans[node.node_id])
+            stats.kernel_launches += len(self.store.tiles)
+            stats.compute_ms += (time.perf_counter() - t_node) * 1e3
+            for a in sorted(node.writes):
+                self.store.bump_local_epoch(a)
+            for a, e in pushes.get(node.node_id, ()):
+                self.exchanges.ensure_round(a, e)
+            stats.nodes_executed += 1
+            stats.node_ms[node.node_id] = (time.perf_counter() - t_node) * 1e3
+        after = self.exchanges.snapshot_stats()
+        for a, n in after["rounds"].items():
+            d = n - before["rounds"].get(a, 0)
+            if d:
+                stats.rounds[a] = d
+        stats.net_messages = after["net_messages"] - before["net_messages"]
+        stats.gpu_launches = self.dev.launches - launches0
+        stats.wall_ms = (time.perf_counter() - t0) * 1e3
+        return stats
+
+    # -- node -> kernel launch ----------------------------------------------
+    def _boxes(self, plan):
+        """(statement index, tile, box lo (local), box extent) for non-empty intersections."""
+        out = []
+        decomp = self.store.decomp
+        for coords in sorted(self.store.tiles):
+            tile = self.store.tiles[coords]
+            for si, ps in enumerate(plan.statements):
+                shape = self.store.arrays[ps.output].shape
+                origin = decomp.tile_origin(shape, coords)
+                ext = decomp.tile_extents(shape)
+                lo, n = [], []
+                for (a, b), o, e in zip(ps.output_slice_bounds, origin, ext):
+                    ia, ib = max(a, o), min(b, o + e)
+                    if ia >= ib:
+                        break
+                    lo.append(ia - o)
+                    n.append(ib - ia)
+                else:
+                    out.append((si, ps, tile, tuple(lo), tuple(n)))
+        return out
+
+    def launch_node(self, node, plan) -> None:
+        boxes = self._boxes(plan)
+        if not boxes:
+            return
+        info = self.store.arrays[plan.statements[0].output]
+        rank, dtype = info.rank, info.dtype
+        src, name, block, smem, n_items, geom, sig = codegen.kernel_source_for(
+            plan, rank, dtype, self.skeleton)
+        kern = self.dev.kernel(src, name, block, smem)
+        items = []
+        for si, ps, tile, lo, n in boxes:
+            out_buf = tile.buffers[ps.output]
+            n3 = (1,) * (3 - rank) + n
+            it = {"out": out_buf.interior_addr(lo), "opy": out_buf.py, "opz": out_buf.pz,
+                  "nx": n3[2], "ny": n3[1], "nz": n3[0], "stmt": si, "in": [], "ipy": [], "ipz": []}
+            # input pointer = element read at offset 0 for the box origin
+            shape = self.store.arrays[ps.output].shape
+            g_lo = [l + o for l, o in zip(lo, self.store.decomp.tile_origin(shape, tile.coords))]
+            for a in ps.inputs:
+                ib = tile.buffers[a]
+                io = self.store.decomp.tile_origin(shape, tile.coords)
+                it["in"].append(ib.interior_addr([g - o for g, o in zip(g_lo, io)]))
+                it["ipy"].append(ib.py)
+                it["ipz"].append(ib.pz)
+            if sig.skeleton == "stream":
+                codegen.stream_item_geometry(it, geom)
+            else:
+                bx, by, _ = block
+                it["bxn"] = -(-n3[2] // bx)
+                it["byn"] = -(-n3[1] // by)
+                it["nzb"] = -(-n3[0] // geom)
+            items.append(it)
+        for k in range(0, len(items), n_items):
+            chunk = items[k:k + n_items]
+            blk = 0
+            for it in chunk:
+                it["blk0"] = blk
+                blk += it["bxn"] * it["byn"] * it["nzb"]
+            params = codegen.pack_items(chunk, sig.max_in, n_items)
+            if self.time_kernels:
+                ev0, ev1 = self.dev.event(), self.dev.event()
+                ev0.record(COMPUTE)
+                self.dev.launch(kern, (blk, 1, 1), params, COMPUTE)
+                ev1.record(COMPUTE)
+                self.kernel_events.append((ev0, ev1))
+            else:
+                self.dev.launch(kern, (blk, 1, 1), params, COMPUTE)
