@@ -141,6 +141,10 @@ class Device:
     def event(self, interprocess: bool = False) -> Event:
         return Event(self, interprocess)
 
+    def open_event(self, handle: bytes) -> Event:
+        """Open a peer process's interprocess event (IPC handle)."""
+        return Event(self, handle=handle)
+
     # -- kernels ------------------------------------------------------------
     def kernel(self, source: str, name: str, block, smem: int = 0) -> Kernel:
         key = (source, name)

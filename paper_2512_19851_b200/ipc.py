@@ -1,0 +1,363 @@
+"""Multi-process GPU workers: one process per GPU, halos over CUDA IPC.
+
+`IpcGpuJob(rank, world, device)` is one worker of an SPMD job (launched by
+torchrun, the driver's bench launcher, or `spawn_local_job` in tests). Every
+rank decodes and executes the same DAG; the block owner map decides which
+tiles each rank owns (grid.py:63-76). torch.distributed (gloo) is used only as
+plumbing: rendezvous, exchanging IPC handles, barriers and host gathers.
+
+The data path never touches the host:
+
+* each rank exports a CUDA IPC memory handle per (tile, array) HBM buffer and
+  IPC event handles for its READY / PULLED event rings (transport.py);
+* halo strips are pulled by the receiver's copy kernel straight out of the
+  owner's mapped buffer (NVLink P2P between GPUs; also works between processes
+  sharing one GPU, which is how the 1-GPU test box exercises this path);
+* the per-round sequence counters live in a shared-memory page (/dev/shm), so
+  the host-side handshake is a few loads/stores, not a socket round trip.
+"""
+
+from __future__ import annotations
+
+import mmap
+import os
+import time
+import uuid
+
+import numpy as np
+
+from .device import Device, PinnedBuffer
+from .exchange import GpuExchangeManager
+from .executor import GpuExecutor
+from .tiles import ArrayInfo, GpuTileStore, TileBuffer, decompose
+from .transport import RING, LocalPeerTransport, TransportAborted
+from .wire import DTYPE_F64
+
+
+class SharedCounters:
+    """int64 [3, world] in /dev/shm: ready_seq, pulled_seq, abort flag."""
+
+    def __init__(self, path: str, world: int, create: bool):
+        self.path = path
+        size = 3 * world * 8
+        if create:
+            with open(path, "wb") as fh:
+                fh.write(b"\xff" * size)  # -1 everywhere
+        self.fh = open(path, "r+b")
+        self.mm = mmap.mmap(self.fh.fileno(), size)
+        self.arr = np.ndarray((3, world), dtype=np.int64, buffer=self.mm)
+        if create:
+            self.arr[2, :] = 0
+
+    def close(self) -> None:
+        try:
+            del self.arr
+            self.mm.close()
+            self.fh.close()
+        except Exception:
+            pass
+
+
+class IpcPeerTransport(LocalPeerTransport):
+    """transport.py protocol over CUDA IPC handles + shared-memory counters."""
+
+    def __init__(self, job: "IpcGpuJob"):
+        self.job = job
+        self.w = job.rank
+        self.store = job.store
+        self.dev = job.dev
+        self.seq = 0
+        self.ready = [self.dev.event(interprocess=True) for _ in range(RING)]
+        self.pulled = [self.dev.event(interprocess=True) for _ in range(RING)]
+        self.readers: dict = {}
+        self.pull_launches = 0
+        self.peer_events: dict = {}
+        self.peer_maps: dict = {}      # (owner, coords, array) -> (layout TileBuffer, addr)
+        self.opened: list = []
+        self.spin_s = 0.0
+
+    # -- handle exchange ---------------------------------------------------------
+    def event_handles(self) -> dict:
+        return {"ready": [e.ipc_handle() for e in self.ready],
+                "pulled": [e.ipc_handle() for e in self.pulled]}
+
+    def open_peer_events(self, table: dict) -> None:
+        for owner, handles in table.items():
+            if owner == self.w:
+                continue
+            self.peer_events[owner] = {k: [self.dev.open_event(h) for h in v]
+                                       for k, v in handles.items()}
+
+    def buffer_table(self) -> dict:
+        out = {}
+        for coords, tile in self.store.tiles.items():
+            for array, buf in tile.buffers.items():
+                out[(tuple(coords), array)] = (self.dev.ipc_handle(buf.ptr), buf.ext[3 - buf.rank:],
+                                               buf.depth[3 - buf.rank:], buf.dtype)
+        return out
+
+    def open_peer_buffers(self, tables: list) -> None:
+        self.close_peer_buffers()
+        for owner, table in enumerate(tables):
+            if owner == self.w:
+                continue
+            for (coords, array), (handle, ext, depth, dtype) in table.items():
+                addr = self.dev.ipc_open(handle)
+                self.opened.append(addr)
+                layout = TileBuffer(self.dev, ext, depth, dtype, ptr=addr)
+                self.peer_maps[(owner, coords, array)] = (layout, addr)
+
+    def close_peer_buffers(self) -> None:
+        for addr in self.opened:
+            try:
+                self.dev.ipc_close(addr)
+            except Exception:
+                pass
+        self.opened.clear()
+        self.peer_maps.clear()
+
+    # -- protocol hooks ----------------------------------------------------------
+    def peer_buffer(self, owner: int, coords, array: int):
+        return self.peer_maps[(owner, tuple(coords), array)]
+
+    def peer_event(self, owner: int, kind: str, slot: int):
+        return self.peer_events[owner][kind][slot]
+
+    def wait_seq(self, owner: int, kind: str, r: int) -> None:
+        row = 0 if kind == "ready" else 1
+        arr = self.job.counters.arr
+        t0 = time.perf_counter()
+        spins = 0
+        while arr[row, owner] < r:
+            if arr[2].any():
+                raise TransportAborted(f"peer aborted while waiting for {kind}[{owner}] >= {r}")
+            spins += 1
+            if spins > 2000:
+                time.sleep(2e-5)
+            if time.perf_counter() - t0 > self.job.timeout_s:
+                raise TransportAborted(f"timeout waiting for {kind}[{owner}] >= {r}")
+        self.spin_s += time.perf_counter() - t0
+
+    def publish(self, kind: str, r: int) -> None:
+        self.job.counters.arr[0 if kind == "ready" else 1, self.w] = r
+
+    def before_realloc(self) -> None:
+        self.dev.sync()
+        self.job.barrier()
+        self.readers.clear()
+        self.close_peer_buffers()
+
+    def after_realloc(self) -> None:
+        self.job.exchange_buffers()
+
+    def abort(self, exc) -> None:
+        self.job.counters.arr[2, self.w] = 1
+
+    def close(self) -> None:
+        self.close_peer_buffers()
+        for evs in self.peer_events.values():
+            for lst in evs.values():
+                for e in lst:
+                    e.close()
+        for e in self.ready + self.pulled:
+            e.close()
+
+
+class IpcGpuJob:
+    """One rank of a multi-process GPU job (same API as session.GpuJob)."""
+
+    def __init__(self, rank: int, world: int, device: int = 0, odf: int = 1,
+                 skeleton: str = "auto", group=None, timeout_s: float = 600.0):
+        import torch.distributed as dist
+
+        self.dist = dist
+        if not dist.is_initialized():
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        self.rank, self.world, self.odf = rank, world, odf
+        self.timeout_s = timeout_s
+        self.dev = Device(device)
+        self.devs = [self.dev]
+        self.skeleton = skeleton
+        self.decomp = None
+        self.store = None
+        self.manager = None
+        self.executor = None
+        self.transport = None
+        self.shapes: dict = {}
+        self.dtypes: dict = {}
+        self._next = 0
+        self._stage = None
+        name = [f"/dev/shm/est-{uuid.uuid4().hex}" if rank == 0 else None]
+        if rank == 0:
+            self.counters = SharedCounters(name[0], world, create=True)
+        dist.broadcast_object_list(name, src=0)
+        if rank != 0:
+            self.counters = SharedCounters(name[0], world, create=False)
+        dist.barrier()
+        if rank == 0:
+            try:
+                os.unlink(name[0])  # mapping stays valid; nothing left behind
+            except OSError:
+                pass
+
+    # -- plumbing ----------------------------------------------------------------
+    def barrier(self) -> None:
+        self.dist.barrier()
+
+    def _all_gather(self, obj) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def exchange_buffers(self) -> None:
+        self.dev.sync()
+        tables = self._all_gather(self.transport.buffer_table())
+        self.transport.open_peer_buffers(tables)
+        self.barrier()
+
+    @property
+    def executors(self) -> list:
+        return [self.executor]
+
+    @property
+    def managers(self) -> list:
+        return [self.manager]
+
+    # -- job API -------------------------------------------------------------
+    def _build(self, shape) -> None:
+        self.decomp = decompose(shape, self.world, self.odf)
+        owners = self.decomp.owner_map(self.world)
+        owned = [c for c, o in owners.items() if o == self.rank]
+        self.store = GpuTileStore(self.dev, self.decomp, owned)
+        self.transport = IpcPeerTransport(self)
+        ev = self._all_gather(self.transport.event_handles())
+        self.transport.open_peer_events(dict(enumerate(ev)))
+        self.manager = GpuExchangeManager(self.store, self.rank, owners, self.transport)
+        self.executor = GpuExecutor(self.store, self.manager, self.skeleton)
+        self.executor.transport = self.transport
+
+    def create_array(self, shape, dtype: int = DTYPE_F64) -> int:
+        shape = tuple(int(e) for e in shape)
+        if self.decomp is None:
+            self._build(shape)
+        aid = self._next
+        self.store.create_array(ArrayInfo(aid, shape, dtype))
+        self._next += 1
+        self.shapes[aid] = shape
+        self.dtypes[aid] = dtype
+        self.exchange_buffers()
+        return aid
+
+    def run(self, dag) -> list:
+        try:
+            return [self.executor.execute_batch(dag)]
+        except BaseException as exc:
+            if self.transport is not None:
+                self.transport.abort(exc)
+            raise
+
+    def sync(self) -> None:
+        self.dev.sync()
+
+    def fetch_local(self, array: int, bounds=None) -> list:
+        self.dev.sync()
+        shape = self.shapes[array]
+        bounds = tuple(bounds) if bounds is not None else tuple((0, e) for e in shape)
+        nbytes = int(np.prod([b - a for a, b in bounds])) * 8
+        if self._stage is None or self._stage.nbytes < nbytes:
+            if self._stage is not None:
+                self._stage.close()
+            self._stage = PinnedBuffer(max(nbytes, 1 << 20))
+        return self.store.gather_slice_pieces(array, bounds, self._stage) if self.store.tiles else []
+
+    def fetch(self, array: int, bounds=None) -> np.ndarray:
+        """Collective: every rank returns the assembled slice."""
+        shape = self.shapes[array]
+        bounds = tuple(bounds) if bounds is not None else tuple((0, e) for e in shape)
+        parts = self._all_gather(self.fetch_local(array, bounds))
+        out = np.zeros([b - a for a, b in bounds], dtype=self.store.fetch_dtype(array))
+        for part in parts:
+            for piece, block in part:
+                out[tuple(slice(a - lo, b - lo) for (a, b), (lo, _) in zip(piece, bounds))] = block
+        return out
+
+    def rounds_by_array(self) -> dict:
+        mine = self.manager.snapshot_stats()["rounds"] if self.store.tiles else None
+        allr = [r for r in self._all_gather(mine) if r is not None]
+        for r in allr[1:]:
+            assert r == allr[0], "ranks disagree on round counts"
+        return allr[0] if allr else {}
+
+    def close(self) -> None:
+        try:
+            self.dev.sync()
+            self.barrier()
+        except Exception:
+            pass
+        if self.transport is not None:
+            self.transport.close()
+        try:
+            self.barrier()
+        except Exception:
+            pass
+        if self.store is not None:
+            self.store.release()
+        if self._stage is not None:
+            self._stage.close()
+        self.counters.close()
+        self.dev.close()
+
+
+def _spawn_entry(rank, world, port, fn, args, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch.distributed as dist
+
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        res = fn(rank, world, *args)
+        q.put((rank, "ok", res))
+    except BaseException as exc:  # report to the parent
+        import traceback
+
+        q.put((rank, "err", traceback.format_exc()))
+    finally:
+        try:
+            dist.destroy_process_group()
+        except Exception:
+            pass
+
+
+def spawn_local_job(world: int, fn, *args, timeout: float = 600.0) -> list:
+    """Run fn(rank, world, *args) in `world` spawned processes; return per-rank results."""
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_spawn_entry, args=(r, world, port, fn, args, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results: dict = {}
+    errors = []
+    deadline = time.time() + timeout
+    while len(results) + len(errors) < world and time.time() < deadline:
+        try:
+            rank, status, payload = q.get(timeout=1.0)
+        except Exception:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
+            continue
+        (results.__setitem__(rank, payload) if status == "ok" else errors.append(payload))
+    for p in procs:
+        p.join(timeout=30)
+        if p.is_alive():
+            p.kill()
+    if errors:
+        raise RuntimeError("worker failed:\n" + errors[0])
+    if len(results) < world:
+        raise RuntimeError(f"only {len(results)}/{world} workers finished")
+    return [results[r] for r in range(world)]

@@ -1,0 +1,110 @@
+"""TEST DOUBLE of device.Device for CPU-only tests of the multi-worker HOST logic
+(prepare/push plan, round sequencing, IPC handshake, realloc barriers).
+
+It performs no computation: allocations are fake addresses, launches and copy
+descriptors are recorded. It lives under tests/ and is injected only by tests;
+the product package has no CPU execution path.
+"""
+
+from __future__ import annotations
+
+import itertools
+
+
+class FakeEvent:
+    def __init__(self, dev, name):
+        self.dev, self.name = dev, name
+
+    def record(self, stream=0):
+        self.dev.log.append(("record", self.name))
+
+    def wait(self, stream=0):
+        self.dev.log.append(("wait", self.name))
+
+    def sync(self):
+        pass
+
+    def done(self):
+        return True
+
+    def elapsed_ms(self, end):
+        return 0.0
+
+    def ipc_handle(self):
+        return self.name.encode().ljust(64, b"\0")
+
+    def close(self):
+        pass
+
+
+class FakeKernel:
+    def __init__(self, name, block, smem):
+        self.fn, self.name, self.block, self.smem = 1, name, tuple(block), smem
+
+
+class FakeDevice:
+    _ids = itertools.count(1)
+
+    def __init__(self, index=0, tag="w"):
+        self.index = index
+        self.tag = tag
+        self.launches = 0
+        self.sm_count = 148
+        self.log: list = []
+        self.copies: list = []
+        self._next = 1 << 40
+        self.allocated: dict = {}
+        self.opened: list = []
+
+    def alloc(self, n):
+        p = self._next
+        self._next += ((n + 4095) // 4096 + 1) * 4096
+        self.allocated[p] = n
+        return p
+
+    def free(self, p):
+        self.allocated.pop(p)
+
+    def memset_zero(self, *a, **k):
+        pass
+
+    def copy_box(self, box, elem, stream=0):
+        self.copies.append(("box", box.src, box.dst, box.nx, box.ny, box.nz))
+
+    def copy_boxes(self, boxes, elem, stream=0):
+        self.launches += 1
+        for b in boxes:
+            self.copies.append(("strip", b.src, b.dst, b.nx, b.ny, b.nz))
+
+    def sync(self):
+        pass
+
+    def stream_sync(self, s):
+        pass
+
+    def event(self, interprocess=False):
+        return FakeEvent(self, f"{self.tag}-ev{next(self._ids)}")
+
+    def open_event(self, handle):
+        return FakeEvent(self, handle.rstrip(b"\0").decode())
+
+    def kernel(self, src, name, block, smem=0):
+        return FakeKernel(name, block, smem)
+
+    def launch(self, k, grid, params, stream=0):
+        self.launches += 1
+        self.log.append(("launch", grid[0]))
+
+    def ipc_handle(self, ptr):
+        return ptr.to_bytes(8, "little") + self.tag.encode().ljust(56, b"\0")
+
+    def ipc_open(self, h):
+        addr = int.from_bytes(h[:8], "little") | (1 << 60)
+        self.opened.append(addr)
+        return addr
+
+    def ipc_close(self, p):
+        self.opened.remove(p)
+
+    def close(self):
+        pass

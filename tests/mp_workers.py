@@ -1,0 +1,77 @@
+"""Per-rank bodies for the multi-process tests (importable by spawned children)."""
+
+from __future__ import annotations
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+for p in (ROOT, os.path.join(ROOT, "tests")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
+def _program(kind: str):
+    from paper_2512_19851_b200.programs import DagProgram, heat3d_program, laplace_program
+
+    prog = DagProgram()
+    if kind == "laplace":
+        names = laplace_program(prog, 32, 10)
+    elif kind == "heat3d":
+        names = heat3d_program(prog, 16, 9, seed_fills=4)
+    else:
+        raise ValueError(kind)
+    return prog, names
+
+
+def _split(dag, size):
+    from paper_2512_19851_b200.ir import Dag, DagNode, compute_edges
+
+    out = []
+    for k in range(0, len(dag.nodes), size):
+        nodes = [DagNode(i, n.statements) for i, n in enumerate(dag.nodes[k:k + size])]
+        out.append(Dag(nodes, compute_edges(nodes), dag.ast_table))
+    return out
+
+
+def host_logic_rank(rank, world, kind, odf, batch):
+    """CPU: fake device, real executor / exchange / IPC transport host logic."""
+    import paper_2512_19851_b200.ipc as ipc
+    from fakedev import FakeDevice
+
+    ipc.Device = lambda device=0: FakeDevice(device, tag=f"r{rank}")
+    from paper_2512_19851_b200.analysis import analyze_dag
+
+    prog, _ = _program(kind)
+    job = ipc.IpcGpuJob(rank, world, odf=odf)
+    for aid in sorted(prog.shapes):
+        job.create_array(prog.shapes[aid])
+    stats = []
+    for part in _split(prog.dag, batch):
+        stats += job.run(part)
+    rounds = job.rounds_by_array()
+    strips = [c for c in job.dev.copies if c[0] == "strip"]
+    out = {"rounds": rounds, "net": sum(s.net_messages for s in stats),
+           "launches": sum(s.kernel_launches for s in stats),
+           "strips": len(strips), "seq": job.transport.seq,
+           "tiles": sorted(job.store.tiles)}
+    job.close()
+    return out
+
+
+def gpu_rank(rank, world, kind, odf, batch):
+    """GPU: real IPC job; several processes may share cuda:0."""
+    from oracle.oracle import bits_equal, reference_execute_dag
+    from paper_2512_19851_b200.ipc import IpcGpuJob
+
+    prog, names = _program(kind)
+    job = IpcGpuJob(rank, world, device=0, odf=odf)
+    for aid in sorted(prog.shapes):
+        job.create_array(prog.shapes[aid])
+    for part in _split(prog.dag, batch):
+        job.run(part)
+    want = reference_execute_dag(prog.dag, prog.shapes)
+    ok = {aid: bits_equal(job.fetch(aid), want[aid]) for aid in prog.shapes}
+    rounds = job.rounds_by_array()
+    job.close()
+    return {"ok": ok, "rounds": rounds}
