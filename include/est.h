@@ -86,6 +86,11 @@ int est_kernel_set_smem(uint64_t fn, int bytes);
 /* Launch fn with ONE by-value parameter struct of params_size bytes. */
 int est_launch(est_ctx *ctx, uint64_t fn, const uint32_t grid[3], const uint32_t block[3],
                uint32_t smem, const void *params, uint32_t params_size, int stream);
+/* TMA descriptor (CUtensorMap, 128 bytes written to out128) for a rank-3
+ * padded tile buffer: dims/strides innermost first; used by the streaming
+ * skeleton's cp.async.bulk.tensor plane loads. */
+int est_tmap_encode_3d(uint64_t base, int elem, const uint64_t dims[3],
+                       const uint64_t strides_bytes[2], const uint32_t box[3], void *out128);
 /* Compile to a cubin image without loading (offline prebuild in build()). */
 int est_nvrtc_compile(const char *src, const char *const *opts, int n_opts, const char *arch,
                       void **image, uint64_t *size);

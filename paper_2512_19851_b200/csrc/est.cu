@@ -65,6 +65,7 @@ extern "C" int est_abi_version(void) { return EST_ABI_VERSION; }
 // driver entry points (resolved lazily through cudart)
 
 struct Driver {
+    decltype(&cuTensorMapEncodeTiled) tensorMapEncodeTiled = nullptr;
     decltype(&cuModuleLoadData) moduleLoadData = nullptr;
     decltype(&cuModuleGetFunction) moduleGetFunction = nullptr;
     decltype(&cuModuleUnload) moduleUnload = nullptr;
@@ -95,6 +96,7 @@ static int driver() {
     rc |= resolve("cuModuleUnload", g_drv.moduleUnload);
     rc |= resolve("cuLaunchKernel", g_drv.launchKernel);
     rc |= resolve("cuFuncSetAttribute", g_drv.funcSetAttribute);
+    rc |= resolve("cuTensorMapEncodeTiled", g_drv.tensorMapEncodeTiled);
     if (rc) return 1;
     g_drv.ok = true;
     return 0;
@@ -479,6 +481,30 @@ extern "C" int est_launch(est_ctx *c, uint64_t fn, const uint32_t grid[3], const
                      CU_LAUNCH_PARAM_BUFFER_SIZE, &sz, CU_LAUNCH_PARAM_END};
     CU_TRY(g_drv.launchKernel((CUfunction)(uintptr_t)fn, grid[0], grid[1], grid[2], block[0],
                               block[1], block[2], smem, (CUstream)pick(c, s), nullptr, extra));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// TMA descriptors for the streaming skeleton
+
+extern "C" int est_tmap_encode_3d(uint64_t base, int elem, const uint64_t dims[3],
+                                  const uint64_t strides_bytes[2], const uint32_t box[3],
+                                  void *out128) {
+    if (driver()) return 1;
+    if (elem != 4 && elem != 8) return fail(14, "elem size %d unsupported", elem);
+    if (base % 16 || strides_bytes[0] % 16 || strides_bytes[1] % 16)
+        return fail(14, "TMA needs 16-byte aligned base and strides");
+    if ((box[0] * (uint32_t)elem) % 16) return fail(14, "TMA box inner extent must be 16-byte multiple");
+    CUtensorMap *tm = reinterpret_cast<CUtensorMap *>(out128);
+    cuuint64_t gdim[3] = {dims[0], dims[1], dims[2]};
+    cuuint64_t gstr[2] = {strides_bytes[0], strides_bytes[1]};
+    cuuint32_t bdim[3] = {box[0], box[1], box[2]};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CU_TRY(g_drv.tensorMapEncodeTiled(
+        tm, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+        (void *)(uintptr_t)base, gdim, gstr, bdim, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
     return 0;
 }
 

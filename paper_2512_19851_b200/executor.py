@@ -23,10 +23,11 @@ kernels actually launched and `device_ms` is CUDA-event time when requested.
 
 from __future__ import annotations
 
+import ctypes as C
 import time
 from dataclasses import dataclass, field
 
-from . import codegen
+from . import _lib, codegen
 from .analysis import analyze_dag, compile_plan
 from .device import COMPUTE
 from .errors import MalformedDag
@@ -72,7 +73,7 @@ class GpuExecutor:
         self.depths: dict = {}
         self.idle_wait = None        # kept for API parity (executor.py:186-189)
         self.skeleton = skeleton     # "auto" | "point" | "stream"
-        self._plan_cache: dict = {}
+        self._tmaps: dict = {}
         self.time_kernels = False    # bracket every node kernel with events
         self.transport = None        # peer transport when the job has >1 worker
         self.kernel_events: list = []
@@ -168,6 +169,46 @@ class GpuExecutor:
         return stats
 
     # -- node -> kernel launch ----------------------------------------------
+    def _tmap(self, buf, box) -> bytes:
+        key = (buf.ptr, buf.py, buf.pz, buf.nz, tuple(box))
+        tm = self._tmaps.get(key)
+        if tm is None:
+            out = (C.c_uint8 * 128)()
+            dims = (C.c_uint64 * 3)(buf.py, buf.pz // buf.py, buf.nz)
+            strides = (C.c_uint64 * 2)(buf.py * buf.elem, buf.pz * buf.elem)
+            bx = (C.c_uint32 * 3)(*box)
+            _lib.check(_lib.load().est_tmap_encode_3d(buf.ptr, buf.elem, dims, strides, bx, out))
+            tm = bytes(out)
+            if len(self._tmaps) > 4096:
+                self._tmaps.clear()
+            self._tmaps[key] = tm
+        return tm
+
+    def _launch_stream(self, kern, sig, geom, it, tile, ps, locals_) -> None:
+        """One stream-skeleton launch for one (tile, statement) box."""
+        local = locals_[0]
+        z, y, x = (0,) * (3 - len(local)) + tuple(local)
+        tmaps, cx, cy, cz = [], [], [], []
+        for s, a in enumerate(ps.inputs):
+            buf = tile.buffers[a]
+            (_r, (w, h), _st, _pl, _off) = geom["slots"][s]
+            tmaps.append(self._tmap(buf, (w, h, 1)))
+            dz, dy, dx = buf.depth
+            cx.append(buf.xoff + x + dx)
+            cy.append(y + dy)
+            cz.append(z + dz)
+        it.update(cx0=cx, cy0=cy, cz0=cz)
+        params = codegen.pack_stream_params(it, tmaps, len(ps.inputs))
+        grid = (it["blocks"], 1, 1)
+        if self.time_kernels:
+            ev0, ev1 = self.dev.event(), self.dev.event()
+            ev0.record(COMPUTE)
+            self.dev.launch(kern, grid, params, COMPUTE)
+            ev1.record(COMPUTE)
+            self.kernel_events.append((ev0, ev1))
+        else:
+            self.dev.launch(kern, grid, params, COMPUTE)
+
     def _boxes(self, plan):
         """(statement index, tile, box lo (local), box extent) for non-empty intersections."""
         out = []
@@ -215,12 +256,17 @@ class GpuExecutor:
                 it["ipz"].append(ib.pz)
             if sig.skeleton == "stream":
                 codegen.stream_item_geometry(it, geom)
+                self._launch_stream(kern, sig, geom, it, tile, ps, [
+                    [g - o for g, o in zip(g_lo, self.store.decomp.tile_origin(shape, tile.coords))]])
+                continue
             else:
                 bx, by, _ = block
                 it["bxn"] = -(-n3[2] // bx)
                 it["byn"] = -(-n3[1] // by)
                 it["nzb"] = -(-n3[0] // geom)
             items.append(it)
+        if sig.skeleton == "stream":
+            return
         for k in range(0, len(items), n_items):
             chunk = items[k:k + n_items]
             blk = 0
