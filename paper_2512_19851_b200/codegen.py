@@ -20,7 +20,7 @@ Skeletons
   up front (ILP), x fastest inside a warp for coalescing. Any rank / offsets /
   multi-statement node (fused statements = separate work items of ONE launch).
 * ``stream`` — rank-3 single-statement nodes whose loads fit a small radius:
-  2.5-D streaming (see STREAM_* below): each CTA owns an (BY x BX) column and
+  2.5-D streaming (stream.py): each CTA owns an (BY x BX) column and
   walks z, staging each input plane (+ halo) in a shared-memory ring so every
   input element is fetched from L2/HBM once per CTA, with the next plane's
   loads issued before the current plane is computed.
@@ -225,185 +225,18 @@ est_node(const __grid_constant__ Params p) {{
 
 
 # --------------------------------------------------------------------------
-# "stream" skeleton (2.5-D) — enabled once measured; see stream_eligible
-
-STREAM_BX = 64          # output columns per CTA (2 warps wide)
-STREAM_BY = 16          # output rows per CTA
-STREAM_TY = 8           # thread rows; each thread computes BY/TY rows
-STREAM_PREFETCH = 4     # planes in flight beyond the stencil's z window
-STREAM_ZCHUNK = 128     # output planes per CTA (z-chunking for parallelism)
-STREAM_MAX_RADIUS = 4
-STREAM_SMEM_BUDGET = 110 * 1024  # keep >= 2 CTAs per SM
-
+# "stream" skeleton (2.5-D, TMA): see stream.py
 
 def stream_eligible(stmts, rank: int, dtype: int = DTYPE_F64) -> bool:
-    if rank != 3 or len(stmts) != 1:
-        return False
-    st = stmts[0]
-    if st.arity == 0:
-        return False
-    rad = slot_radius(st)
-    if any(max(r) > STREAM_MAX_RADIUS for r in rad.values()):
-        return False
-    return _stream_layout(st, dtype)[3] <= STREAM_SMEM_BUDGET
+    from . import stream
 
-
-def _stream_layout(st: StmtSig, dtype: int):
-    """Per slot: (rz, ry, rx), box (w, h), stages; total smem bytes."""
-    elem = ELEM[dtype]
-    rad = slot_radius(st)
-    slots = []
-    total = 0
-    for s in range(st.arity):
-        rz, ry, rx = rad.get(s, (0, 0, 0))
-        q = 16 // elem
-        w = -(-(STREAM_BX + 2 * rx) // q) * q
-        h = STREAM_BY + 2 * ry
-        stages = 2 * rz + 1 + STREAM_PREFETCH
-        plane = -(-(w * h * elem) // 1024) * 1024
-        slots.append(((rz, ry, rx), (w, h), stages, plane, total))
-        total += stages * plane
-    bars = 8 * sum(s[2] for s in slots)
-    return slots, bars, total, total + bars + 1024
+    return stream.eligible(stmts, rank, dtype)
 
 
 def stream_source(sig: NodeSig, rank: int) -> tuple:
-    """2.5-D streaming skeleton: TMA plane loads into per-slot smem rings.
+    from . import stream
 
-    CTA = (STREAM_BX x STREAM_BY) output column walking STREAM_ZCHUNK planes.
-    Thread 0 is the TMA producer: each input plane tile (+halo) is one
-    cp.async.bulk.tensor.3d into a ring stage, completion tracked by that
-    stage's mbarrier (expect_tx). Every thread waits for the planes its window
-    needs, evaluates the plan reading all operands from shared memory, stores
-    its outputs with coalesced st.global, and after a CTA barrier the freed
-    stage is refilled STREAM_PREFETCH planes ahead.
-    """
-    st = sig.stmts[0]
-    T = CTYPE[sig.dtype]
-    slots, bar_bytes, data_bytes, smem = _stream_layout(st, sig.dtype)
-    n_in = st.arity
-    rows = STREAM_BY // STREAM_TY
-    pre = [f"// generated by paper_2512_19851_b200/codegen.py — skeleton \"stream\" (TMA 2.5-D)",
-           f"typedef {T} T;",
-           "struct __align__(64) Tmap { unsigned long long w[16]; };",
-           f"struct __align__(64) Params {{ Tmap tm[{n_in}];",
-           "  unsigned long long out; long long opy, opz, nx, ny, nz, zc, nbx, nby, nzc;",
-           f"  long long cx0[{n_in}], cy0[{n_in}], cz0[{n_in}]; }};",
-           "__device__ __forceinline__ unsigned smem_u32(const void* p) {",
-           "  return (unsigned)__cvta_generic_to_shared(p); }",
-           "__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned n) {",
-           "  asm volatile(\"mbarrier.init.shared::cta.b64 [%0], %1;\" :: \"r\"(smem_u32(b)), \"r\"(n)); }",
-           "__device__ __forceinline__ void mbar_expect(unsigned long long* b, unsigned bytes) {",
-           "  asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(smem_u32(b)), \"r\"(bytes) : \"memory\"); }",
-           "__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {",
-           "  asm volatile(\"{\\n .reg .pred p;\\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\\n\"",
-           "               \" @!p bra W;\\n}\" :: \"r\"(smem_u32(b)), \"r\"(parity) : \"memory\"); }",
-           "__device__ __forceinline__ void tma_load3(void* dst, const Tmap* tm, int x, int y, int z, unsigned long long* b) {",
-           "  asm volatile(\"cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\"",
-           "               :: \"r\"(smem_u32(dst)), \"l\"(tm), \"r\"(x), \"r\"(y), \"r\"(z), \"r\"(smem_u32(b)) : \"memory\"); }",
-           ]
-    body = []
-    body.append(f"extern \"C\" __global__ void __launch_bounds__({STREAM_BX * STREAM_TY})")
-    body.append("est_stream(const __grid_constant__ Params p) {")
-    body.append("  extern __shared__ __align__(1024) unsigned char smem[];")
-    body.append(f"  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + {data_bytes});")
-    body.append("  long long b = blockIdx.x;")
-    body.append("  const long long bx = b % p.nbx; b /= p.nbx;")
-    body.append("  const long long by = b % p.nby; const long long bzc = b / p.nby;")
-    body.append(f"  const long long x0 = bx * {STREAM_BX}, y0 = by * {STREAM_BY};")
-    body.append("  const long long zs = bzc * p.zc;")
-    body.append("  const long long ze = (zs + p.zc < p.nz) ? zs + p.zc : p.nz;")
-    body.append("  const int tx = threadIdx.x, ty = threadIdx.y;")
-    body.append("  const bool leader = (tx == 0 && ty == 0);")
-    # barrier offsets per slot
-    bar_off = 0
-    for s, (_r, _b, stages, _plane, _o) in enumerate(slots):
-        body.append(f"  unsigned long long* bar{s} = bars + {bar_off};")
-        bar_off += stages
-    body.append("  if (leader) {")
-    for s in range(n_in):
-        body.append(f"    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm[{s}]) : \"memory\");")
-    body.append(f"    for (int i = 0; i < {bar_off}; ++i) mbar_init(bars + i, 1);")
-    body.append("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
-    body.append("  }")
-    body.append("  __syncthreads();")
-    # prologue: slot s's ring is filled with input planes q in [-rz, -rz + stages)
-    body.append("  if (leader) {")
-    for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
-        body.append(f"    for (long long q = -{rz}; q < -{rz} + {stages} && q < (ze - zs) + {rz}; ++q) {{")
-        body.append(f"      const int stg = (int)(q + {rz});")
-        body.append(f"      mbar_expect(bar{s} + stg, {w * h * ELEM[sig.dtype]});")
-        body.append(f"      tma_load3(smem + {off} + stg * {plane}, &p.tm[{s}], (int)(p.cx0[{s}] + x0 - {rx}),"
-                    f" (int)(p.cy0[{s}] + y0 - {ry}), (int)(p.cz0[{s}] + zs + q), bar{s} + stg);")
-        body.append("    }")
-    body.append("  }")
-    # per slot: next plane to issue = -rz + stages; track via per-slot loop below using generic q
-    body.append("  for (long long z = 0; z < ze - zs; ++z) {")
-    # wait for planes needed: for slot s, planes z-rz..z+rz; the newest is z+rz; older waited already
-    for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
-        body.append(f"    {{ const long long q = z + {rz}; const int k = (int)(q + {rz});")
-        body.append(f"      if (z == 0) {{ for (int kk = 0; kk <= 2 * {rz}; ++kk) mbar_wait(bar{s} + (kk % {stages}), (kk / {stages}) & 1); }}")
-        body.append(f"      else mbar_wait(bar{s} + (k % {stages}), (k / {stages}) & 1); }}")
-    # compute rows
-    for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
-        body.append(f"    const {T}* ring{s} = reinterpret_cast<const {T}*>(smem + {off});")
-    body.append(f"    T* __restrict__ o = reinterpret_cast<T*>(p.out);")
-    body.append(f"    #pragma unroll")
-    body.append(f"    for (int r = 0; r < {rows}; ++r) {{")
-    body.append(f"      const int ly = ty + r * {STREAM_TY};")
-    body.append("      const long long gx = x0 + tx, gy = y0 + ly;")
-
-    def load(slot, off3):
-        dz, dy, dx = off3
-        (rz, ry, rx), (w, h), stages, plane, _o = slots[slot]
-        return (f"ring{slot}[(int)(((z + {rz + dz}) % {stages}) * {plane // ELEM[sig.dtype]})"
-                f" + (ly + {ry + dy}) * {w} + (tx + {rx + dx})]")
-
-    lines, res = _emit_expr(st, sig.dtype, load)
-    body.append("      if (gx < p.nx && gy < p.ny) {")
-    body += ["        " + ln for ln in lines]
-    body.append(f"        o[(zs + z) * p.opz + gy * p.opy + gx] = {res};")
-    body.append("      }")
-    body.append("    }")
-    body.append("    __syncthreads();  // every thread is done with plane z - rz of each ring")
-    body.append("    if (leader) {")
-    body.append("      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");")
-    for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
-        # plane freed for slot s: q_free = z - rz; refill with q_free + stages (issued per slot)
-        body.append(f"      {{ const long long qn = z - {rz} + {stages}; if (qn < (ze - zs) + {rz}) {{")
-        body.append(f"          const int k = (int)(qn + {rz}); const int stg = k % {stages};")
-        body.append(f"          unsigned long long* bb = bar{s} + stg;")
-        body.append(f"          mbar_expect(bb, {w * h * ELEM[sig.dtype]});")
-        body.append(f"          tma_load3(smem + {off} + stg * {plane}, &p.tm[{s}], (int)(p.cx0[{s}] + x0 - {rx}),"
-                    f" (int)(p.cy0[{s}] + y0 - {ry}), (int)(p.cz0[{s}] + zs + qn), bb); }} }}")
-    body.append("    }")
-    body.append("  }")
-    body.append("}")
-    src = "\n".join(pre) + "\n" + "\n".join(body) + "\n"
-    geom = {"slots": slots, "smem": smem}
-    return src, "est_stream", (STREAM_BX, STREAM_TY, 1), smem, 1, geom
-
-
-def stream_item_geometry(item: dict, geom) -> None:
-    """Grid shape of one stream item (z-chunked xy tiles)."""
-    item["nbx"] = -(-item["nx"] // STREAM_BX)
-    item["nby"] = -(-item["ny"] // STREAM_BY)
-    item["zc"] = min(STREAM_ZCHUNK, item["nz"])
-    item["nzc"] = -(-item["nz"] // item["zc"])
-    item["blocks"] = item["nbx"] * item["nby"] * item["nzc"]
-
-
-def pack_stream_params(item: dict, tmaps: list, n_in: int) -> bytes:
-    out = bytearray()
-    for tm in tmaps:
-        assert len(tm) == 128
-        out += tm
-    out += struct.pack("<Qqqqqqqqqq", item["out"], item["opy"], item["opz"], item["nx"], item["ny"],
-                       item["nz"], item["zc"], item["nbx"], item["nby"], item["nzc"])
-    out += struct.pack(f"<{n_in}q", *item["cx0"]) + struct.pack(f"<{n_in}q", *item["cy0"])
-    out += struct.pack(f"<{n_in}q", *item["cz0"])
-    pad = (-len(out)) % 64
-    return bytes(out) + b"\0" * pad
+    return stream.source(sig, rank)
 
 
 # --------------------------------------------------------------------------

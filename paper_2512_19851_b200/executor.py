@@ -23,11 +23,10 @@ kernels actually launched and `device_ms` is CUDA-event time when requested.
 
 from __future__ import annotations
 
-import ctypes as C
 import time
 from dataclasses import dataclass, field
 
-from . import _lib, codegen
+from . import codegen, stream
 from .analysis import analyze_dag, compile_plan
 from .device import COMPUTE
 from .errors import MalformedDag
@@ -173,12 +172,8 @@ class GpuExecutor:
         key = (buf.ptr, buf.py, buf.pz, buf.nz, tuple(box))
         tm = self._tmaps.get(key)
         if tm is None:
-            out = (C.c_uint8 * 128)()
-            dims = (C.c_uint64 * 3)(buf.py, buf.pz // buf.py, buf.nz)
-            strides = (C.c_uint64 * 2)(buf.py * buf.elem, buf.pz * buf.elem)
-            bx = (C.c_uint32 * 3)(*box)
-            _lib.check(_lib.load().est_tmap_encode_3d(buf.ptr, buf.elem, dims, strides, bx, out))
-            tm = bytes(out)
+            tm = self.dev.tmap_3d(buf.ptr, buf.elem, (buf.py, buf.pz // buf.py, buf.nz),
+                                  (buf.py * buf.elem, buf.pz * buf.elem), box)
             if len(self._tmaps) > 4096:
                 self._tmaps.clear()
             self._tmaps[key] = tm
@@ -198,7 +193,7 @@ class GpuExecutor:
             cy.append(y + dy)
             cz.append(z + dz)
         it.update(cx0=cx, cy0=cy, cz0=cz)
-        params = codegen.pack_stream_params(it, tmaps, len(ps.inputs))
+        params = stream.pack_params(it, tmaps, len(ps.inputs))
         grid = (it["blocks"], 1, 1)
         if self.time_kernels:
             ev0, ev1 = self.dev.event(), self.dev.event()
@@ -255,7 +250,7 @@ class GpuExecutor:
                 it["ipy"].append(ib.py)
                 it["ipz"].append(ib.pz)
             if sig.skeleton == "stream":
-                codegen.stream_item_geometry(it, geom)
+                stream.item_geometry(it)
                 self._launch_stream(kern, sig, geom, it, tile, ps, [
                     [g - o for g, o in zip(g_lo, self.store.decomp.tile_origin(shape, tile.coords))]])
                 continue

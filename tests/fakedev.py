@@ -95,6 +95,9 @@ class FakeDevice:
         self.launches += 1
         self.log.append(("launch", grid[0]))
 
+    def tmap_3d(self, base, elem, dims, strides, box):
+        return base.to_bytes(8, "little").ljust(128, b"\0")
+
     def ipc_handle(self, ptr):
         return ptr.to_bytes(8, "little") + self.tag.encode().ljust(56, b"\0")
 
