@@ -250,7 +250,7 @@ class GpuExecutor:
                 it["ipy"].append(ib.py)
                 it["ipz"].append(ib.pz)
             if sig.skeleton == "stream":
-                stream.item_geometry(it)
+                stream.item_geometry(it, self.dev.sm_count, smem)
                 self._launch_stream(kern, sig, geom, it, tile, ps, [
                     [g - o for g, o in zip(g_lo, self.store.decomp.tile_origin(shape, tile.coords))]])
                 continue

@@ -164,21 +164,32 @@ class IpcPeerTransport(LocalPeerTransport):
 
 
 class IpcGpuJob:
-    """One rank of a multi-process GPU job (same API as session.GpuJob)."""
+    """One rank of a multi-process GPU job (same API as session.GpuJob).
+
+    `group` is the host plumbing (hostgroup.GlooGroup by default, or the
+    worker's PeerGroup); `decomp` may be imposed (the coordinator's fixed
+    decomposition, grid.py:43-117) instead of derived from the first shape.
+    """
 
     def __init__(self, rank: int, world: int, device: int = 0, odf: int = 1,
-                 skeleton: str = "auto", group=None, timeout_s: float = 600.0):
-        import torch.distributed as dist
+                 skeleton: str = "auto", group=None, timeout_s: float = 600.0,
+                 decomp=None, owner_map: dict | None = None):
+        if group is None:
+            import torch.distributed as dist
 
-        self.dist = dist
-        if not dist.is_initialized():
-            dist.init_process_group("gloo", rank=rank, world_size=world)
+            if not dist.is_initialized():
+                dist.init_process_group("gloo", rank=rank, world_size=world)
+            from .hostgroup import GlooGroup
+
+            group = GlooGroup()
+        self.group = group
         self.rank, self.world, self.odf = rank, world, odf
         self.timeout_s = timeout_s
         self.dev = Device(device)
         self.devs = [self.dev]
         self.skeleton = skeleton
-        self.decomp = None
+        self.decomp = decomp
+        self.owner_map = owner_map
         self.store = None
         self.manager = None
         self.executor = None
@@ -187,27 +198,31 @@ class IpcGpuJob:
         self.dtypes: dict = {}
         self._next = 0
         self._stage = None
-        name = [f"/dev/shm/est-{uuid.uuid4().hex}" if rank == 0 else None]
-        if rank == 0:
-            self.counters = SharedCounters(name[0], world, create=True)
-        dist.broadcast_object_list(name, src=0)
-        if rank != 0:
-            self.counters = SharedCounters(name[0], world, create=False)
-        dist.barrier()
-        if rank == 0:
+        self.counters = None
+        self._open_counters()
+        if decomp is not None:
+            self._build(None)
+
+    def _open_counters(self) -> None:
+        name = f"/dev/shm/est-{uuid.uuid4().hex}" if self.rank == 0 else None
+        if self.rank == 0:
+            self.counters = SharedCounters(name, self.world, create=True)
+        name = self.group.allgather(name)[0]
+        if self.rank != 0:
+            self.counters = SharedCounters(name, self.world, create=False)
+        self.group.barrier()
+        if self.rank == 0:
             try:
-                os.unlink(name[0])  # mapping stays valid; nothing left behind
+                os.unlink(name)  # mappings stay valid; nothing is left behind
             except OSError:
                 pass
 
     # -- plumbing ----------------------------------------------------------------
     def barrier(self) -> None:
-        self.dist.barrier()
+        self.group.barrier()
 
     def _all_gather(self, obj) -> list:
-        out = [None] * self.world
-        self.dist.all_gather_object(out, obj)
-        return out
+        return self.group.allgather(obj)
 
     def exchange_buffers(self) -> None:
         self.dev.sync()
@@ -225,8 +240,10 @@ class IpcGpuJob:
 
     # -- job API -------------------------------------------------------------
     def _build(self, shape) -> None:
-        self.decomp = decompose(shape, self.world, self.odf)
-        owners = self.decomp.owner_map(self.world)
+        if self.decomp is None:
+            self.decomp = decompose(shape, self.world, self.odf)
+        owners = self.owner_map or self.decomp.owner_map(self.world)
+        self.owner_map = owners
         owned = [c for c, o in owners.items() if o == self.rank]
         self.store = GpuTileStore(self.dev, self.decomp, owned)
         self.transport = IpcPeerTransport(self)
@@ -236,13 +253,13 @@ class IpcGpuJob:
         self.executor = GpuExecutor(self.store, self.manager, self.skeleton)
         self.executor.transport = self.transport
 
-    def create_array(self, shape, dtype: int = DTYPE_F64) -> int:
+    def create_array(self, shape, dtype: int = DTYPE_F64, array: int | None = None) -> int:
         shape = tuple(int(e) for e in shape)
-        if self.decomp is None:
+        if self.store is None:
             self._build(shape)
-        aid = self._next
+        aid = self._next if array is None else int(array)
         self.store.create_array(ArrayInfo(aid, shape, dtype))
-        self._next += 1
+        self._next = max(self._next, aid + 1)
         self.shapes[aid] = shape
         self.dtypes[aid] = dtype
         self.exchange_buffers()
@@ -268,7 +285,9 @@ class IpcGpuJob:
             if self._stage is not None:
                 self._stage.close()
             self._stage = PinnedBuffer(max(nbytes, 1 << 20))
-        return self.store.gather_slice_pieces(array, bounds, self._stage) if self.store.tiles else []
+        if self.store is None or not self.store.tiles:
+            return []
+        return self.store.gather_slice_pieces(array, bounds, self._stage)
 
     def fetch(self, array: int, bounds=None) -> np.ndarray:
         """Collective: every rank returns the assembled slice."""
@@ -304,7 +323,8 @@ class IpcGpuJob:
             self.store.release()
         if self._stage is not None:
             self._stage.close()
-        self.counters.close()
+        if self.counters is not None:
+            self.counters.close()
         self.dev.close()
 
 
