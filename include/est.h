@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define EST_ABI_VERSION 3
+#define EST_ABI_VERSION 4
 
 typedef struct est_ctx est_ctx;       /* one device + compute/copy streams      */
 typedef struct est_module est_module; /* an NVRTC-compiled, loaded cubin        */
@@ -87,10 +87,12 @@ int est_kernel_set_smem(uint64_t fn, int bytes);
 int est_launch(est_ctx *ctx, uint64_t fn, const uint32_t grid[3], const uint32_t block[3],
                uint32_t smem, const void *params, uint32_t params_size, int stream);
 /* TMA descriptor (CUtensorMap, 128 bytes written to out128) for a rank-3
- * padded tile buffer: dims/strides innermost first; used by the streaming
- * skeleton's cp.async.bulk.tensor plane loads. */
+ * padded tile buffer: dims/strides innermost first; l2_promotion 0 none,
+ * 1 64B, 2 128B, 3 256B. Used by the streaming skeleton's
+ * cp.async.bulk.tensor plane loads. */
 int est_tmap_encode_3d(uint64_t base, int elem, const uint64_t dims[3],
-                       const uint64_t strides_bytes[2], const uint32_t box[3], void *out128);
+                       const uint64_t strides_bytes[2], const uint32_t box[3], int l2_promotion,
+                       void *out128);
 /* Compile to a cubin image without loading (offline prebuild in build()). */
 int est_nvrtc_compile(const char *src, const char *const *opts, int n_opts, const char *arch,
                       void **image, uint64_t *size);

@@ -14,7 +14,7 @@ from .errors import from_code
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libest.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 u64, i64, i32, u32 = C.c_uint64, C.c_int64, C.c_int, C.c_uint32
 vp = C.c_void_p
@@ -50,7 +50,7 @@ _SIGS = {
     "est_module_destroy": (i32, [vp]),
     "est_kernel_set_smem": (i32, [u64, i32]),
     "est_launch": (i32, [vp, u64, P(u32), P(u32), u32, vp, u32, i32]),
-    "est_tmap_encode_3d": (i32, [u64, i32, P(u64), P(u64), P(u32), vp]),
+    "est_tmap_encode_3d": (i32, [u64, i32, P(u64), P(u64), P(u32), i32, vp]),
     "est_nvrtc_compile":(i32, [C.c_char_p, P(C.c_char_p), i32, C.c_char_p, P(vp), P(u64)]),
     "est_buffer_free": (None, [vp]),
     "est_event_create": (i32, [vp, i32, P(vp)]),

@@ -250,7 +250,9 @@ def kernel_source_for(plan, rank: int, dtype: int, skeleton: str = "auto") -> tu
 
     Memoised on the plan instructions, so repeated nodes cost a dict lookup.
     """
-    key = (tuple(p.instructions for p in plan.statements), rank, dtype, skeleton)
+    from . import stream
+
+    key = (tuple(p.instructions for p in plan.statements), rank, dtype, skeleton, stream.DEFAULT)
     hit = _SRC_CACHE.get(key)
     if hit is not None:
         return hit

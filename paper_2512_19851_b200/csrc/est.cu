@@ -489,8 +489,12 @@ extern "C" int est_launch(est_ctx *c, uint64_t fn, const uint32_t grid[3], const
 
 extern "C" int est_tmap_encode_3d(uint64_t base, int elem, const uint64_t dims[3],
                                   const uint64_t strides_bytes[2], const uint32_t box[3],
-                                  void *out128) {
+                                  int l2_promotion, void *out128) {
     if (driver()) return 1;
+    static const CUtensorMapL2promotion promo[4] = {
+        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+    if (l2_promotion < 0 || l2_promotion > 3) return fail(14, "l2_promotion must be 0..3");
     if (elem != 4 && elem != 8) return fail(14, "elem size %d unsupported", elem);
     if (base % 16 || strides_bytes[0] % 16 || strides_bytes[1] % 16)
         return fail(14, "TMA needs 16-byte aligned base and strides");
@@ -503,7 +507,7 @@ extern "C" int est_tmap_encode_3d(uint64_t base, int elem, const uint64_t dims[3
     CU_TRY(g_drv.tensorMapEncodeTiled(
         tm, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
         (void *)(uintptr_t)base, gdim, gstr, bdim, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_SWIZZLE_NONE, promo[l2_promotion],
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
     return 0;
 }

@@ -176,12 +176,12 @@ class Device:
         check(self.lib.est_launch(self.ctx, k.fn, g, b, k.smem, params, len(params), stream))
         self.launches += 1
 
-    def tmap_3d(self, base: int, elem: int, dims, strides_bytes, box) -> bytes:
+    def tmap_3d(self, base: int, elem: int, dims, strides_bytes, box, l2_promotion: int = 3) -> bytes:
         """128-byte CUtensorMap for a rank-3 buffer (innermost dimension first)."""
         out = (C.c_uint8 * 128)()
         check(self.lib.est_tmap_encode_3d(int(base), elem, (C.c_uint64 * 3)(*dims),
                                           (C.c_uint64 * 2)(*strides_bytes),
-                                          (C.c_uint32 * 3)(*box), out))
+                                          (C.c_uint32 * 3)(*box), int(l2_promotion), out))
         return bytes(out)
 
     # -- ipc ----------------------------------------------------------------

@@ -168,12 +168,12 @@ class GpuExecutor:
         return stats
 
     # -- node -> kernel launch ----------------------------------------------
-    def _tmap(self, buf, box) -> bytes:
-        key = (buf.ptr, buf.py, buf.pz, buf.nz, tuple(box))
+    def _tmap(self, buf, box, l2promo: int = 3) -> bytes:
+        key = (buf.ptr, buf.py, buf.pz, buf.nz, tuple(box), l2promo)
         tm = self._tmaps.get(key)
         if tm is None:
             tm = self.dev.tmap_3d(buf.ptr, buf.elem, (buf.py, buf.pz // buf.py, buf.nz),
-                                  (buf.py * buf.elem, buf.pz * buf.elem), box)
+                                  (buf.py * buf.elem, buf.pz * buf.elem), box, l2promo)
             if len(self._tmaps) > 4096:
                 self._tmaps.clear()
             self._tmaps[key] = tm
@@ -187,7 +187,7 @@ class GpuExecutor:
         for s, a in enumerate(ps.inputs):
             buf = tile.buffers[a]
             (_r, (w, h), _st, _pl, _off) = geom["slots"][s]
-            tmaps.append(self._tmap(buf, (w, h, 1)))
+            tmaps.append(self._tmap(buf, (w, h, 1), geom["cfg"].l2promo))
             dz, dy, dx = buf.depth
             cx.append(buf.xoff + x + dx)
             cy.append(y + dy)
@@ -250,7 +250,7 @@ class GpuExecutor:
                 it["ipy"].append(ib.py)
                 it["ipz"].append(ib.pz)
             if sig.skeleton == "stream":
-                stream.item_geometry(it, self.dev.sm_count, smem)
+                stream.item_geometry(it, self.dev.sm_count, geom)
                 self._launch_stream(kern, sig, geom, it, tile, ps, [
                     [g - o for g, o in zip(g_lo, self.store.decomp.tile_origin(shape, tile.coords))]])
                 continue

@@ -253,6 +253,11 @@ class IpcGpuJob:
         self.executor = GpuExecutor(self.store, self.manager, self.skeleton)
         self.executor.transport = self.transport
 
+    def set_owner_map(self, owners: dict) -> None:
+        """Swap the tile -> worker map after a migration (worker.py:374-377)."""
+        self.owner_map = dict(owners)
+        self.manager.owner_map = self.owner_map
+
     def create_array(self, shape, dtype: int = DTYPE_F64, array: int | None = None) -> int:
         shape = tuple(int(e) for e in shape)
         if self.store is None:

@@ -4,17 +4,17 @@ For rank-3 single-statement nodes (the 3-D heat/Jacobi sweeps that dominate
 the BASELINE configs) every input element must cross HBM once and every
 output once (16 B per update in fp64). The skeleton:
 
-* work item = a BX x BY column of the output box over ZCHUNK planes; a
-  PERSISTENT grid (one wave: SMs x resident CTAs) walks the items round-robin,
-  item = blockIdx.x + k * gridDim.x with x-tiles fastest, so the CTAs working
-  on xy-neighbours of the same z-range run concurrently and the halo rows /
-  columns they share are L2 hits instead of extra HBM reads;
+* work item = a BX x BY column of the output box over ZCHUNK planes. Either
+  one CTA per item (`persistent=False`) or a persistent one-wave grid walking
+  items round-robin (x-tiles fastest) — both are kept because which one keeps
+  the shared halo rows in L2 is a measured property (profiles/);
 * per input slot s with z-radius rz a ring of 2*rz+1+PREFETCH shared-memory
   stages holds one input plane tile plus its (ry, rx) halo; each stage is ONE
   `cp.async.bulk.tensor.3d` (TMA) issued by a single elected thread and
   completed on the stage's mbarrier (expect_tx). The TMA box starts at a
-  16-byte aligned x coordinate (hardware requirement; the sub-16 B shift is
-  applied to the shared-memory column index);
+  16-byte aligned x coordinate (a hardware requirement found with
+  scripts/probes/tma_probe.cu; the sub-16 B shift goes into the shared-memory
+  column index);
 * every thread evaluates the postorder plan (codegen._emit_expr) for BY/TY
   rows of the current plane from shared memory with compile-time offsets and
   stores with coalesced st.global (x fastest);
@@ -25,24 +25,43 @@ output once (16 B per update in fp64). The skeleton:
 
 from __future__ import annotations
 
+import os
 import struct
+from dataclasses import dataclass
 
 from .codegen import CTYPE, ELEM, NodeSig, StmtSig, _emit_expr, slot_radius
 from .wire import DTYPE_F64
 
-import os
-
-BX = int(os.environ.get("EST_STREAM_BX", 64))          # output columns per CTA
-BY = int(os.environ.get("EST_STREAM_BY", 16))          # output rows per CTA
-TY = int(os.environ.get("EST_STREAM_TY", 8))           # thread rows (BY // TY rows each)
-PREFETCH = int(os.environ.get("EST_STREAM_PREFETCH", 4))  # planes in flight past the window
 MIN_ZCHUNK = 32
 MAX_RADIUS = 4
-SMEM_BUDGET = 110 * 1024
+SMEM_BUDGET = 150 * 1024
 SMEM_PER_SM = 228 * 1024
 
 
-def layout(st: StmtSig, dtype: int):
+@dataclass(frozen=True)
+class StreamCfg:
+    bx: int = 64            # output columns per CTA
+    by: int = 16            # output rows per CTA
+    ty: int = 8             # thread rows; each thread computes by // ty rows
+    prefetch: int = 4       # planes in flight beyond the stencil's z window
+    persistent: bool = False
+    zchunk: int = 128       # planes per item when not persistent
+    l2promo: int = 3        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
+
+
+def _env_cfg() -> StreamCfg:
+    e = os.environ.get
+    return StreamCfg(bx=int(e("EST_STREAM_BX", 64)), by=int(e("EST_STREAM_BY", 16)),
+                     ty=int(e("EST_STREAM_TY", 8)), prefetch=int(e("EST_STREAM_PREFETCH", 4)),
+                     persistent=e("EST_STREAM_PERSISTENT", "0") == "1",
+                     zchunk=int(e("EST_STREAM_ZCHUNK", 128)),
+                     l2promo=int(e("EST_STREAM_L2PROMO", 3)))
+
+
+DEFAULT = _env_cfg()
+
+
+def layout(st: StmtSig, dtype: int, cfg: StreamCfg):
     """Per slot: ((rz, ry, rx), (w, h), stages, plane_bytes, offset); data bytes; total."""
     elem = ELEM[dtype]
     q = 16 // elem
@@ -50,9 +69,9 @@ def layout(st: StmtSig, dtype: int):
     slots, off = [], 0
     for s in range(st.arity):
         rz, ry, rx = rad.get(s, (0, 0, 0))
-        w = -(-(BX + 2 * rx + q - 1) // q) * q   # room for the 16-byte alignment shift
-        h = BY + 2 * ry
-        stages = 2 * rz + 1 + PREFETCH
+        w = -(-(cfg.bx + 2 * rx + q - 1) // q) * q   # room for the 16-byte alignment shift
+        h = cfg.by + 2 * ry
+        stages = 2 * rz + 1 + cfg.prefetch
         plane = -(-(w * h * elem) // 1024) * 1024
         slots.append(((rz, ry, rx), (w, h), stages, plane, off))
         off += stages * plane
@@ -60,16 +79,20 @@ def layout(st: StmtSig, dtype: int):
     return slots, off, off + 8 * n_bars + 1024
 
 
-def eligible(stmts, rank: int, dtype: int = DTYPE_F64) -> bool:
+def eligible(stmts, rank: int, dtype: int = DTYPE_F64, cfg: StreamCfg | None = None) -> bool:
+    cfg = cfg or DEFAULT
     if rank != 3 or len(stmts) != 1 or stmts[0].arity == 0:
         return False
-    if any(max(r) > MAX_RADIUS for r in slot_radius(stmts[0]).values()):
+    rad = slot_radius(stmts[0]).values()
+    if any(max(r) > MAX_RADIUS for r in rad):
         return False
-    return layout(stmts[0], dtype)[2] <= SMEM_BUDGET
+    if any((cfg.bx + 2 * r[2] + 2) > 256 or (cfg.by + 2 * r[1]) > 256 for r in rad):
+        return False  # TMA box extents are limited to 256 elements
+    return layout(stmts[0], dtype, cfg)[2] <= SMEM_BUDGET
 
 
-def blocks_per_sm(smem: int) -> int:
-    return max(1, min(SMEM_PER_SM // (smem + 1024), 2048 // (BX * TY)))
+def blocks_per_sm(smem: int, cfg: StreamCfg) -> int:
+    return max(1, min(SMEM_PER_SM // (smem + 1024), 2048 // (cfg.bx * cfg.ty)))
 
 
 _PTX_HELPERS = r"""
@@ -93,17 +116,19 @@ __device__ __forceinline__ void tma_load3(void* dst, const void* tm, int x, int 
 """
 
 
-def source(sig: NodeSig, rank: int) -> tuple:
+def source(sig: NodeSig, rank: int, cfg: StreamCfg | None = None) -> tuple:
+    cfg = cfg or DEFAULT
+    BX, BY, TY = cfg.bx, cfg.by, cfg.ty
     st = sig.stmts[0]
     T = CTYPE[sig.dtype]
     elem = ELEM[sig.dtype]
     q = 16 // elem
-    slots, data_bytes, smem = layout(st, sig.dtype)
+    slots, data_bytes, smem = layout(st, sig.dtype, cfg)
     n_in = st.arity
     rpt = BY // TY
     L = []
     a = L.append
-    a('// generated by paper_2512_19851_b200/stream.py — skeleton "stream" (TMA 2.5-D, persistent)')
+    a(f'// generated by paper_2512_19851_b200/stream.py — skeleton "stream" (TMA 2.5-D) {cfg}')
     a(f"typedef {T} T;")
     a("struct __align__(64) Tmap { unsigned long long w[16]; };")
     a(f"struct __align__(64) Params {{ Tmap tm[{n_in}];")
@@ -201,7 +226,7 @@ def source(sig: NodeSig, rank: int) -> tuple:
     a("  }")
     a("}")
     src = "\n".join(L) + "\n"
-    return src, "est_stream", (BX, TY, 1), smem, 1, {"slots": slots, "smem": smem}
+    return src, "est_stream", (BX, TY, 1), smem, 1, {"slots": slots, "smem": smem, "cfg": cfg}
 
 
 def _choose_zchunks(nz: int, n_xy: int, capacity: int) -> int:
@@ -211,22 +236,26 @@ def _choose_zchunks(nz: int, n_xy: int, capacity: int) -> int:
         zc = -(-nz // nzc)
         items = n_xy * nzc
         rounds = -(-items // capacity)
-        balance = items / (rounds * capacity)
-        eff = balance * zc / (zc + 2)  # ~2 halo planes re-read per chunk
+        eff = items / (rounds * capacity) * zc / (zc + 2)  # ~2 halo planes re-read per chunk
         if eff > best_eff + 1e-9:
             best, best_eff = nzc, eff
     return best
 
 
-def item_geometry(item: dict, sm_count: int, smem: int) -> None:
-    item["nbx"] = -(-item["nx"] // BX)
-    item["nby"] = -(-item["ny"] // BY)
-    cap = sm_count * blocks_per_sm(smem)
-    nzc = _choose_zchunks(item["nz"], item["nbx"] * item["nby"], cap)
-    item["zc"] = -(-item["nz"] // nzc)
+def item_geometry(item: dict, sm_count: int, geom: dict) -> None:
+    cfg = geom["cfg"]
+    item["nbx"] = -(-item["nx"] // cfg.bx)
+    item["nby"] = -(-item["ny"] // cfg.by)
+    n_xy = item["nbx"] * item["nby"]
+    if cfg.persistent:
+        cap = sm_count * blocks_per_sm(geom["smem"], cfg)
+        nzc = _choose_zchunks(item["nz"], n_xy, cap)
+        item["zc"] = -(-item["nz"] // nzc)
+    else:
+        item["zc"] = min(cfg.zchunk, item["nz"])
     item["nzc"] = -(-item["nz"] // item["zc"])
-    n_items = item["nbx"] * item["nby"] * item["nzc"]
-    item["blocks"] = min(n_items, cap)
+    n_items = n_xy * item["nzc"]
+    item["blocks"] = min(n_items, sm_count * blocks_per_sm(geom["smem"], cfg)) if cfg.persistent else n_items
 
 
 def pack_params(item: dict, tmaps: list, n_in: int) -> bytes:

@@ -95,7 +95,7 @@ class FakeDevice:
         self.launches += 1
         self.log.append(("launch", grid[0]))
 
-    def tmap_3d(self, base, elem, dims, strides, box):
+    def tmap_3d(self, base, elem, dims, strides, box, l2_promotion=3):
         return base.to_bytes(8, "little").ljust(128, b"\0")
 
     def ipc_handle(self, ptr):
