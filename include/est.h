@@ -86,6 +86,13 @@ int est_kernel_set_smem(uint64_t fn, int bytes);
 /* Launch fn with ONE by-value parameter struct of params_size bytes. */
 int est_launch(est_ctx *ctx, uint64_t fn, const uint32_t grid[3], const uint32_t block[3],
                uint32_t smem, const void *params, uint32_t params_size, int stream);
+/* CUDA graphs: capture every launch of a batch once on a stream, replay it as
+ * one graph launch (host batch path). */
+typedef struct est_graph est_graph;
+int est_graph_begin(est_ctx *ctx, int stream);
+int est_graph_end(est_ctx *ctx, int stream, est_graph **out);
+int est_graph_launch(est_ctx *ctx, est_graph *graph, int stream);
+int est_graph_destroy(est_graph *graph);
 /* TMA descriptor (CUtensorMap, 128 bytes written to out128) for a rank-3
  * padded tile buffer: dims/strides innermost first; l2_promotion 0 none,
  * 1 64B, 2 128B, 3 256B. Used by the streaming skeleton's

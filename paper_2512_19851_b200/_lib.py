@@ -50,6 +50,10 @@ _SIGS = {
     "est_module_destroy": (i32, [vp]),
     "est_kernel_set_smem": (i32, [u64, i32]),
     "est_launch": (i32, [vp, u64, P(u32), P(u32), u32, vp, u32, i32]),
+    "est_graph_begin": (i32, [vp, i32]),
+    "est_graph_end": (i32, [vp, i32, P(vp)]),
+    "est_graph_launch": (i32, [vp, vp, i32]),
+    "est_graph_destroy": (i32, [vp]),
     "est_tmap_encode_3d": (i32, [u64, i32, P(u64), P(u64), P(u32), i32, vp]),
     "est_nvrtc_compile":(i32, [C.c_char_p, P(C.c_char_p), i32, C.c_char_p, P(vp), P(u64)]),
     "est_buffer_free": (None, [vp]),

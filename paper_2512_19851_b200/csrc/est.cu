@@ -485,6 +485,50 @@ extern "C" int est_launch(est_ctx *c, uint64_t fn, const uint32_t grid[3], const
 }
 
 // ---------------------------------------------------------------------------
+// CUDA graphs: a whole batch's launches captured once and replayed
+
+struct est_graph {
+    cudaGraphExec_t exec;
+    int device;
+};
+
+extern "C" int est_graph_begin(est_ctx *c, int s) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamBeginCapture(pick(c, s), cudaStreamCaptureModeThreadLocal));
+    return 0;
+}
+
+extern "C" int est_graph_end(est_ctx *c, int s, est_graph **out) {
+    *out = nullptr;
+    CUDA_TRY(cudaSetDevice(c->device));
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaStreamEndCapture(pick(c, s), &g));
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(1, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+    est_graph *eg = new est_graph();
+    eg->exec = exec;
+    eg->device = c->device;
+    *out = eg;
+    return 0;
+}
+
+extern "C" int est_graph_launch(est_ctx *c, est_graph *g, int s) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaGraphLaunch(g->exec, pick(c, s)));
+    return 0;
+}
+
+extern "C" int est_graph_destroy(est_graph *g) {
+    if (!g) return 0;
+    cudaSetDevice(g->device);
+    cudaGraphExecDestroy(g->exec);
+    delete g;
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
 // TMA descriptors for the streaming skeleton
 
 extern "C" int est_tmap_encode_3d(uint64_t base, int elem, const uint64_t dims[3],

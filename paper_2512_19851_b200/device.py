@@ -80,6 +80,23 @@ class Event:
             self.ptr = C.c_void_p()
 
 
+class Graph:
+    """An instantiated CUDA graph (one batch's launches), replayable."""
+
+    def __init__(self, dev: "Device", ptr):
+        self.dev, self.ptr = dev, ptr
+        self.kernels = 0
+
+    def launch(self, stream: int = COMPUTE) -> None:
+        check(_lib.load().est_graph_launch(self.dev.ctx, self.ptr, stream))
+        self.dev.launches += self.kernels
+
+    def close(self) -> None:
+        if self.ptr:
+            _lib.load().est_graph_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+
 class Kernel:
     __slots__ = ("fn", "name", "block", "smem")
 
@@ -175,6 +192,15 @@ class Device:
         b = (C.c_uint32 * 3)(*k.block)
         check(self.lib.est_launch(self.ctx, k.fn, g, b, k.smem, params, len(params), stream))
         self.launches += 1
+
+    # -- CUDA graphs ----------------------------------------------------------
+    def graph_begin(self, stream: int = COMPUTE) -> None:
+        check(self.lib.est_graph_begin(self.ctx, stream))
+
+    def graph_end(self, stream: int = COMPUTE) -> "Graph":
+        g = C.c_void_p()
+        check(self.lib.est_graph_end(self.ctx, stream, C.byref(g)))
+        return Graph(self, g)
 
     def tmap_3d(self, base: int, elem: int, dims, strides_bytes, box, l2_promotion: int = 3) -> bytes:
         """128-byte CUtensorMap for a rank-3 buffer (innermost dimension first)."""

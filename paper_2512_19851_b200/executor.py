@@ -76,6 +76,9 @@ class GpuExecutor:
         self.time_kernels = False    # bracket every node kernel with events
         self.transport = None        # peer transport when the job has >1 worker
         self.kernel_events: list = []
+        self.graphs = True           # replay repeated batches as CUDA graphs
+        self._replay: dict = {}
+        self.replays = 0
 
     # -- preparation (executor.py:193-256) ----------------------------------
     def prepare_batch(self, dag):
@@ -127,8 +130,104 @@ class GpuExecutor:
                 last_writer[a] = node.node_id
         return metas, plans, pushes
 
+    # -- host batch path: replay cache ------------------
+    def _state_sig(self) -> tuple:
+        st, ex = self.store, self.exchanges
+        return (st.version, tuple(sorted(
+            (a, st.local_epoch(a) == 0, ex.ghost_generation(a) == st.local_epoch(a),
+             self.depths.get(a)) for a in st.arrays)))
+
+    def execute_batch(self, dag, key: bytes | None = None) -> BatchStats:
+        """Run one batch. With `key` (e.g. a digest of the DAG bytes) a batch
+        whose DAG and epoch / layout state repeat is replayed from a captured
+        CUDA graph instead of being re-analysed and re-launched node by node;
+        the epoch / round bookkeeping is applied exactly as a fresh run would."""
+        if key is None or not self.graphs or self.transport is not None or self.time_kernels:
+            return self._execute(dag)
+        sig = (key, self._state_sig())
+        ent = self._replay.get(sig)
+        if ent is not None and ent.get("graph") is not None:
+            return self._replay_batch(ent)
+        t0 = time.perf_counter()
+        before = self._epoch_snapshot()
+        capture = ent is not None  # second sighting: kernels compiled, buffers stable
+        if capture:
+            launches0 = self.dev.launches
+            self.dev.graph_begin(COMPUTE)
+            try:
+                stats = self._execute(dag)
+            except BaseException:
+                try:
+                    self.dev.graph_end(COMPUTE).close()
+                except Exception:
+                    pass
+                raise
+            graph = self.dev.graph_end(COMPUTE)
+            graph.kernels = self.dev.launches - launches0
+            self.dev.launches = launches0
+            graph.launch(COMPUTE)
+            ent["graph"] = graph
+        else:
+            stats = self._execute(dag)
+        after = self._epoch_snapshot()
+        if self._state_sig()[0] != sig[1][0]:
+            return stats  # buffers were reallocated: not a steady-state batch
+        if not capture:
+            self._replay[sig] = {"effects": self._effects(before, after), "stats": stats}
+        stats.wall_ms = (time.perf_counter() - t0) * 1e3
+        return stats
+
+    def _epoch_snapshot(self) -> dict:
+        st, ex = self.store, self.exchanges
+        return {a: (st.local_epoch(a), ex.ghost_generation(a), ex.rounds_started.get(a, 0))
+                for a in st.arrays} | {None: ex.net_messages}
+
+    @staticmethod
+    def _effects(before: dict, after: dict) -> dict:
+        eff = {}
+        for a, val in before.items():
+            if a is None:
+                continue
+            l0, g0, r0 = val
+            l1, g1, r1 = after[a]
+            eff[a] = (l1 - l0, None if g1 == g0 else g1 - l0, r1 - r0)
+        eff[None] = after[None] - before[None]
+        return eff
+
+    def _replay_batch(self, ent: dict) -> BatchStats:
+        t0 = time.perf_counter()
+        ent["graph"].launch(COMPUTE)
+        st, ex = self.store, self.exchanges
+        for a, e in ent["effects"].items():
+            if a is None:
+                ex.net_messages += e
+                continue
+            dl, grel, dr = e
+            start = st.local_epoch(a)
+            for tile in st.tiles.values():
+                tile.local_epoch[a] += dl
+            if grel is not None:
+                ex.completed[a] = start + grel
+                for tile in st.tiles.values():
+                    tile.ghost_epoch[a] = start + grel
+            if dr:
+                ex.rounds_started[a] = ex.rounds_started.get(a, 0) + dr
+        s = ent["stats"]
+        out = BatchStats(nodes_executed=s.nodes_executed, kernel_launches=s.kernel_launches,
+                         rounds=dict(s.rounds), net_messages=s.net_messages,
+                         gpu_launches=ent["graph"].kernels)
+        out.wall_ms = (time.perf_counter() - t0) * 1e3
+        self.replays += 1
+        return out
+
+    def drop_replays(self) -> None:
+        for ent in self._replay.values():
+            if ent.get("graph") is not None:
+                ent["graph"].close()
+        self._replay.clear()
+
     # -- execution (executor.py:258-348) ------------------------------------
-    def execute_batch(self, dag) -> BatchStats:
+    def _execute(self, dag) -> BatchStats:
         t0 = time.perf_counter()
         before = self.exchanges.snapshot_stats()
         launches0 = self.dev.launches

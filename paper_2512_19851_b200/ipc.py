@@ -198,6 +198,7 @@ class IpcGpuJob:
         self.dtypes: dict = {}
         self._next = 0
         self._stage = None
+        self._decoded: dict = {}
         self.counters = None
         self._open_counters()
         if decomp is not None:
@@ -270,7 +271,17 @@ class IpcGpuJob:
         self.exchange_buffers()
         return aid
 
-    def run(self, dag) -> list:
+    def run_bytes(self, blob: bytes) -> list:
+        from .wire import decode_dag
+
+        dag = self._decoded.get(blob)
+        if dag is None:
+            dag = self._decoded[blob] = decode_dag(blob)
+            if len(self._decoded) > 64:
+                self._decoded.clear()
+        return self.run(dag)
+
+    def run(self, dag, key: bytes | None = None) -> list:
         try:
             return [self.executor.execute_batch(dag)]
         except BaseException as exc:

@@ -40,6 +40,7 @@ class GpuJob:
         self.shapes: dict = {}
         self.dtypes: dict = {}
         self._stage = None
+        self._decoded: dict = {}
 
     def _build(self, shape) -> None:
         self.decomp = decompose(shape, self.workers, self.odf)
@@ -73,9 +74,27 @@ class GpuJob:
         self.dtypes[aid] = dtype
         return aid
 
-    def run(self, dag) -> list:
+    def run_bytes(self, blob: bytes) -> list:
+        """Execute a batch given as DAG bytes (the W_BATCH payload).
+
+        Repeated batches skip decode and, on a single worker, replay a captured
+        CUDA graph (executor.GpuExecutor.execute_batch `key`)."""
+        import hashlib
+
+        from .wire import decode_dag
+
+        key = hashlib.blake2b(blob, digest_size=16).digest()
+        dag = self._decoded.get(key)
+        if dag is None:
+            dag = decode_dag(blob)
+            if len(self._decoded) > 64:
+                self._decoded.clear()
+            self._decoded[key] = dag
+        return self.run(dag, key)
+
+    def run(self, dag, key: bytes | None = None) -> list:
         if self.workers == 1:
-            return [self.executors[0].execute_batch(dag)]
+            return [self.executors[0].execute_batch(dag, key)]
         results = [None] * self.workers
         errors = []
 
@@ -127,6 +146,8 @@ class GpuJob:
         return counts[0] if counts else {}
 
     def close(self) -> None:
+        for ex in self.executors:
+            ex.drop_replays()
         if self._stage is not None:
             self._stage.close()
             self._stage = None

@@ -40,22 +40,30 @@ SMEM_PER_SM = 228 * 1024
 
 @dataclass(frozen=True)
 class StreamCfg:
+    """Tile / pipeline shape. Defaults = best of the measured sweep
+    (profiles/r1_stream_sweep.md): 64x8 tiles, one row per thread."""
+
     bx: int = 64            # output columns per CTA
-    by: int = 16            # output rows per CTA
+    by: int = 8             # output rows per CTA
     ty: int = 8             # thread rows; each thread computes by // ty rows
     prefetch: int = 4       # planes in flight beyond the stencil's z window
     persistent: bool = False
     zchunk: int = 128       # planes per item when not persistent
-    l2promo: int = 3        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
+    l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
+    ws: bool = False        # warp-specialised: dedicated TMA producer warp, full/empty mbarriers
+    zreg: bool = False      # (ws only) pure-z offsets of the thread's own column from registers
 
 
 def _env_cfg() -> StreamCfg:
     e = os.environ.get
-    return StreamCfg(bx=int(e("EST_STREAM_BX", 64)), by=int(e("EST_STREAM_BY", 16)),
-                     ty=int(e("EST_STREAM_TY", 8)), prefetch=int(e("EST_STREAM_PREFETCH", 4)),
+    d = StreamCfg()
+    return StreamCfg(bx=int(e("EST_STREAM_BX", d.bx)), by=int(e("EST_STREAM_BY", d.by)),
+                     ty=int(e("EST_STREAM_TY", d.ty)), prefetch=int(e("EST_STREAM_PREFETCH", d.prefetch)),
                      persistent=e("EST_STREAM_PERSISTENT", "0") == "1",
-                     zchunk=int(e("EST_STREAM_ZCHUNK", 128)),
-                     l2promo=int(e("EST_STREAM_L2PROMO", 3)))
+                     zchunk=int(e("EST_STREAM_ZCHUNK", d.zchunk)),
+                     l2promo=int(e("EST_STREAM_L2PROMO", d.l2promo)),
+                     ws=e("EST_STREAM_WS", "1" if d.ws else "0") == "1",
+                     zreg=e("EST_STREAM_ZREG", "1" if d.zreg else "0") == "1")
 
 
 DEFAULT = _env_cfg()
@@ -75,7 +83,7 @@ def layout(st: StmtSig, dtype: int, cfg: StreamCfg):
         plane = -(-(w * h * elem) // 1024) * 1024
         slots.append(((rz, ry, rx), (w, h), stages, plane, off))
         off += stages * plane
-    n_bars = sum(s[2] for s in slots)
+    n_bars = sum(s[2] for s in slots) * (2 if cfg.ws else 1)
     return slots, off, off + 8 * n_bars + 1024
 
 
@@ -91,8 +99,12 @@ def eligible(stmts, rank: int, dtype: int = DTYPE_F64, cfg: StreamCfg | None = N
     return layout(stmts[0], dtype, cfg)[2] <= SMEM_BUDGET
 
 
+def threads_per_cta(cfg: StreamCfg) -> int:
+    return cfg.bx * cfg.ty + (32 if cfg.ws else 0)
+
+
 def blocks_per_sm(smem: int, cfg: StreamCfg) -> int:
-    return max(1, min(SMEM_PER_SM // (smem + 1024), 2048 // (cfg.bx * cfg.ty)))
+    return max(1, min(SMEM_PER_SM // (smem + 1024), 2048 // threads_per_cta(cfg)))
 
 
 _PTX_HELPERS = r"""
@@ -118,6 +130,8 @@ __device__ __forceinline__ void tma_load3(void* dst, const void* tm, int x, int 
 
 def source(sig: NodeSig, rank: int, cfg: StreamCfg | None = None) -> tuple:
     cfg = cfg or DEFAULT
+    if cfg.ws:
+        return source_ws(sig, rank, cfg)
     BX, BY, TY = cfg.bx, cfg.by, cfg.ty
     st = sig.stmts[0]
     T = CTYPE[sig.dtype]
@@ -227,6 +241,180 @@ def source(sig: NodeSig, rank: int, cfg: StreamCfg | None = None) -> tuple:
     a("}")
     src = "\n".join(L) + "\n"
     return src, "est_stream", (BX, TY, 1), smem, 1, {"slots": slots, "smem": smem, "cfg": cfg}
+
+
+def source_ws(sig: NodeSig, rank: int, cfg: StreamCfg) -> tuple:
+    """Warp-specialised variant: one producer warp (lane 0) streams planes with
+    TMA through FULL (expect_tx) / EMPTY (one arrive per compute warp)
+    mbarriers per ring stage; compute warps never meet at a CTA barrier and run
+    ahead into the next item while the producer keeps PREFETCH planes in
+    flight. With `zreg` each thread keeps its own column's pure-z operands
+    (offsets (dz,0,0)) in registers, rotating one plane per step."""
+    BX, BY, TY = cfg.bx, cfg.by, cfg.ty
+    st = sig.stmts[0]
+    T = CTYPE[sig.dtype]
+    elem = ELEM[sig.dtype]
+    q = 16 // elem
+    slots, data_bytes, smem = layout(st, sig.dtype, cfg)
+    n_in = st.arity
+    rpt = BY // TY
+    CT = BX * TY
+    NW = CT // 32
+    assert CT % 32 == 0
+    loads = [ins for ins in st.instructions if ins[0] == "load"]
+    zreg_slots = set()
+    if cfg.zreg:
+        for s in range(n_in):
+            if any(i[1] == s and i[2][1] == 0 and i[2][2] == 0 for i in loads):
+                zreg_slots.add(s)
+    L = []
+    a = L.append
+    a(f'// generated by paper_2512_19851_b200/stream.py — skeleton "stream" (TMA 2.5-D, warp-specialised) {cfg}')
+    a(f"typedef {T} T;")
+    a("struct __align__(64) Tmap { unsigned long long w[16]; };")
+    a(f"struct __align__(64) Params {{ Tmap tm[{n_in}];")
+    a("  unsigned long long out; long long opy, opz, nx, ny, nz, zc, nbx, nby, nzc;")
+    a(f"  long long cx0[{n_in}], cy0[{n_in}], cz0[{n_in}]; }};")
+    L.append(_PTX_HELPERS)
+    a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
+    a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
+    a(f'extern "C" __global__ void __launch_bounds__({CT + 32})')
+    a("est_stream(const __grid_constant__ Params p) {")
+    a("  extern __shared__ __align__(1024) unsigned char smem[];")
+    a(f"  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + {data_bytes});")
+    a("  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;")
+    a("  const int nbx = (int)p.nbx, nby = (int)p.nby;")
+    a("  const int n_items = nbx * nby * (int)p.nzc;")
+    nb = 0
+    for s, (_r, _wh, stages, _pl, off) in enumerate(slots):
+        a(f"  unsigned long long* full{s} = bars + {nb};")
+        a(f"  unsigned long long* empty{s} = bars + {nb + stages};")
+        a(f"  const {T}* ring{s} = reinterpret_cast<const {T}*>(smem + {off});")
+        nb += 2 * stages
+    a("  if (tid == 0) {")
+    for s, (_r, _wh, stages, _pl, _off) in enumerate(slots):
+        a(f"    for (int i = 0; i < {stages}; ++i) {{ mbar_init(full{s} + i, 1); mbar_init(empty{s} + i, {NW}); }}")
+    a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
+    a("  }")
+    a("  __syncthreads();")
+    # ---------------- producer warp
+    a(f"  if (warp == {NW}) {{")
+    a("    if (lane != 0) return;")
+    for s in range(n_in):
+        a(f"    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm[{s}]) : \"memory\");")
+    for s in range(n_in):
+        a(f"    int fill{s} = 0;")
+    a("    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+    a("      const int bx = item % nbx, rest = item / nbx;")
+    a("      const int by = rest % nby, bzc = rest / nby;")
+    a(f"      const int x0 = bx * {BX}, y0 = by * {BY};")
+    a("      const int zs = bzc * (int)p.zc;")
+    a("      const int nzl = ((zs + (int)p.zc) < (int)p.nz ? (int)p.zc : (int)p.nz - zs);")
+    maxr = max(s[0][0] for s in slots)
+    a(f"      for (int k = 0; k < nzl + {2 * maxr}; ++k) {{")
+    for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
+        a(f"        if (k < nzl + {2 * rz}) {{")
+        a(f"          const int g = fill{s} + k, stg = g % {stages};")
+        a(f"          if (g >= {stages}) mbar_wait(empty{s} + stg, ((g / {stages}) - 1) & 1);")
+        a(f"          const int xs = (int)p.cx0[{s}] + x0 - {rx};")
+        a(f"          mbar_expect(full{s} + stg, {w * h * elem});")
+        a(f"          tma_load3(smem + {off} + stg * {plane}, &p.tm[{s}], xs - (xs & {q - 1}),"
+          f" (int)p.cy0[{s}] + y0 - {ry}, (int)p.cz0[{s}] + zs + k - {rz}, full{s} + stg);")
+        a("        }")
+    a("      }")
+    for s, ((rz, _ry, _rx), _wh, _stg, _pl, _off) in enumerate(slots):
+        a(f"      fill{s} += nzl + {2 * rz};")
+    a("    }")
+    a("    return;")
+    a("  }")
+    # ---------------- compute warps
+    a(f"  const int tx = tid % {BX}, ty = tid / {BX};")
+    for s in range(n_in):
+        a(f"  int fill{s} = 0;")
+    for s in sorted(zreg_slots):
+        rz = slots[s][0][0]
+        a(f"  T cz{s}[{rpt}][{2 * rz + 1}];")
+    a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+    a("    const int bx = item % nbx, rest = item / nbx;")
+    a("    const int by = rest % nby, bzc = rest / nby;")
+    a(f"    const int x0 = bx * {BX}, y0 = by * {BY};")
+    a("    const int zs = bzc * (int)p.zc;")
+    a("    const int nzl = ((zs + (int)p.zc) < (int)p.nz ? (int)p.zc : (int)p.nz - zs);")
+    for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
+        a(f"    const int sh{s} = ((int)p.cx0[{s}] + x0 - {rx}) & {q - 1};")
+    a(f"    T* __restrict__ orow = reinterpret_cast<T*>(p.out) + (long long)zs * p.opz"
+      f" + (long long)(y0 + ty) * p.opy + (x0 + tx);")
+    a("    const bool colok = (x0 + tx) < (int)p.nx;")
+    a("    for (int z = 0; z < nzl; ++z) {")
+    for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
+        a("      if (z == 0) {")
+        a(f"        for (int k = 0; k <= {2 * rz}; ++k) {{ const int g = fill{s} + k;"
+          f" mbar_wait(full{s} + g % {stages}, (g / {stages}) & 1); }}")
+        a("      } else {")
+        a(f"        const int g = fill{s} + z + {2 * rz}; mbar_wait(full{s} + g % {stages}, (g / {stages}) & 1);")
+        a("      }")
+    need: dict = {}
+    for ins in loads:
+        s, (dz, dy, dx) = ins[1], ins[2]
+        if s in zreg_slots and dy == 0 and dx == 0:
+            continue
+        need.setdefault(s, set()).add(dz)
+    for s in zreg_slots:
+        rz = slots[s][0][0]
+        need.setdefault(s, set()).update(range(-rz, rz + 1))  # register fill at z == 0 + newest plane
+    for s, dzs in sorted(need.items()):
+        (rz, ry, rx), (w, h), stages, plane, off = slots[s]
+        for dz in sorted(dzs):
+            nm = f"P{s}_{'m' if dz < 0 else 'p'}{abs(dz)}"
+            a(f"      const {T}* {nm} = ring{s} + ((fill{s} + z + {rz + dz}) % {stages}) * {plane // elem}"
+              f" + ty * {w} + tx + sh{s};")
+    for s in sorted(zreg_slots):
+        (rz, ry, rx), (w, h), _stg, _pl, _o = slots[s]
+        ctr = ry * w + rx
+        a("      #pragma unroll")
+        a(f"      for (int r = 0; r < {rpt}; ++r) {{")
+        a("        if (z == 0) {")
+        for dz in range(-rz, rz):
+            nm = f"P{s}_{'m' if dz < 0 else 'p'}{abs(dz)}"
+            a(f"          cz{s}[r][{dz + rz}] = {nm}[r * {TY * w} + {ctr}];")
+        a("        }")
+        nm = f"P{s}_p{rz}" if rz > 0 else f"P{s}_p0"
+        a(f"        cz{s}[r][{2 * rz}] = {nm}[r * {TY * w} + {ctr}];")
+        a("      }")
+
+    def load(slot, off3):
+        dz, dy, dx = off3
+        (rz, ry, rx), (w, h), _stg, _pl, _o = slots[slot]
+        if slot in zreg_slots and dy == 0 and dx == 0:
+            return f"cz{slot}[r][{dz + rz}]"
+        nm = f"P{slot}_{'m' if dz < 0 else 'p'}{abs(dz)}"
+        return f"{nm}[r * {TY * w} + {(ry + dy) * w + (rx + dx)}]"
+
+    lines, res = _emit_expr(st, sig.dtype, load)
+    a("      #pragma unroll")
+    a(f"      for (int r = 0; r < {rpt}; ++r) {{")
+    a(f"        if (colok && (y0 + ty + r * {TY}) < (int)p.ny) {{")
+    for ln in lines:
+        a("          " + ln)
+    a(f"          orow[(long long)r * {TY} * p.opy] = {res};")
+    a("        }")
+    for s in sorted(zreg_slots):
+        rz = slots[s][0][0]
+        for d in range(2 * rz):
+            a(f"        cz{s}[r][{d}] = cz{s}[r][{d + 1}];")
+    a("      }")
+    a("      orow += p.opz;")
+    a("      __syncwarp();")
+    for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
+        a(f"      if (lane == 0) mbar_arrive(empty{s} + (fill{s} + z) % {stages});  // plane k = z is dead")
+    a("    }")
+    for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
+        a(f"    for (int k = nzl; k < nzl + {2 * rz}; ++k) if (lane == 0) mbar_arrive(empty{s} + (fill{s} + k) % {stages});")
+        a(f"    fill{s} += nzl + {2 * rz};")
+    a("  }")
+    a("}")
+    src = "\n".join(L) + "\n"
+    return src, "est_stream", (CT + 32, 1, 1), smem, 1, {"slots": slots, "smem": smem, "cfg": cfg}
 
 
 def _choose_zchunks(nz: int, n_xy: int, capacity: int) -> int:

@@ -186,6 +186,7 @@ class GpuTileStore:
         self.decomp = decomp
         self.tiles: dict = {c: GpuTile(c) for c in owned}
         self.arrays: dict = {}
+        self.version = 0  # bumped whenever any buffer is (re)allocated or dropped
 
     # -- creation / capacity ------------------------------------------------
     def create_array(self, info: ArrayInfo) -> None:
@@ -195,6 +196,7 @@ class GpuTileStore:
             raise InvalidShape(f"bad dtype {info.dtype}")
         self.decomp.check_divisible(info.shape)
         self.arrays[info.array] = info
+        self.version += 1
         ext = self.decomp.tile_extents(info.shape)
         zero = (0,) * info.rank
         for tile in self.tiles.values():
@@ -227,6 +229,8 @@ class GpuTileStore:
             tile.buffers[array] = dst
             tile.depths[array] = new
             grew = True
+        if grew:
+            self.version += 1
         return grew
 
     def fetch_dtype(self, array: int):

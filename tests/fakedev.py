@@ -111,3 +111,30 @@ class FakeDevice:
 
     def close(self):
         pass
+
+
+class FakeGraph:
+    def __init__(self, dev):
+        self.dev = dev
+        self.kernels = 0
+        self.launched = 0
+
+    def launch(self, stream=0):
+        self.launched += 1
+        self.dev.launches += self.kernels
+
+    def close(self):
+        pass
+
+
+def _graph_begin(self, stream=0):
+    self.capturing = True
+
+
+def _graph_end(self, stream=0):
+    self.capturing = False
+    return FakeGraph(self)
+
+
+FakeDevice.graph_begin = _graph_begin
+FakeDevice.graph_end = _graph_end
