@@ -40,18 +40,19 @@ SMEM_PER_SM = 228 * 1024
 
 @dataclass(frozen=True)
 class StreamCfg:
-    """Tile / pipeline shape. Defaults = best of the measured sweep
-    (profiles/r1_stream_sweep.md): 64x8 tiles, one row per thread."""
+    """Tile / pipeline shape. Defaults = best of the measured sweeps under
+    sustained (power-capped) load (profiles/r1_stream_sweep.md): 128x8 tiles,
+    2 rows per thread, warp-specialised producer, z-register rotation."""
 
-    bx: int = 64            # output columns per CTA
+    bx: int = 128           # output columns per CTA
     by: int = 8             # output rows per CTA
-    ty: int = 8             # thread rows; each thread computes by // ty rows
-    prefetch: int = 4       # planes in flight beyond the stencil's z window
+    ty: int = 4             # thread rows; each thread computes by // ty rows
+    prefetch: int = 3       # planes in flight beyond the stencil's z window
     persistent: bool = False
     zchunk: int = 128       # planes per item when not persistent
     l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
-    ws: bool = False        # warp-specialised: dedicated TMA producer warp, full/empty mbarriers
-    zreg: bool = False      # (ws only) pure-z offsets of the thread's own column from registers
+    ws: bool = True         # warp-specialised: dedicated TMA producer warp, full/empty mbarriers
+    zreg: bool = True       # (ws only) pure-z offsets of the thread's own column from registers
 
 
 def _env_cfg() -> StreamCfg:

@@ -19,20 +19,22 @@ from paper_2512_19851_b200.session import GpuJob  # noqa: E402
 from paper_2512_19851_b200.stream import StreamCfg  # noqa: E402
 
 N = int(os.environ.get("SWEEP_N", 1024))
-B = StreamCfg(bx=64, by=8, ty=8, prefetch=3, zchunk=128, l2promo=2)
+B = StreamCfg(bx=128, by=8, ty=4, prefetch=3, zchunk=128, l2promo=2, ws=True, zreg=True)
+R = dict(zchunk=128, l2promo=2, ws=True, zreg=True)
 CFGS = {
-    "S0_H2_p3": B,
-    "S1_H0_p4": StreamCfg(bx=64, by=8, ty=8, prefetch=4, l2promo=2),
-    "S2_ws_p3": StreamCfg(ws=True, prefetch=3),
-    "S3_ws_p4": StreamCfg(ws=True, prefetch=4),
-    "S4_ws_p6": StreamCfg(ws=True, prefetch=6),
-    "S5_ws_zreg_p3": StreamCfg(ws=True, zreg=True, prefetch=3),
-    "S6_ws_zreg_p4": StreamCfg(ws=True, zreg=True, prefetch=4),
-    "S7_ws_zreg_16x8_p3": StreamCfg(ws=True, zreg=True, by=16, ty=8, prefetch=3),
-    "S8_ws_zreg_128x8_p3": StreamCfg(ws=True, zreg=True, bx=128, by=8, ty=4, prefetch=3),
-    "S9_ws_zreg_persist_p4": StreamCfg(ws=True, zreg=True, prefetch=4, persistent=True),
-    "S10_ws_zreg_z256_p4": StreamCfg(ws=True, zreg=True, prefetch=4, zchunk=256),
-    "S11_ws_zreg_16x16_p3": StreamCfg(ws=True, zreg=True, by=16, ty=16, prefetch=3),
+    "T0_S8": B,
+    "T1_p4": StreamCfg(bx=128, by=8, ty=4, prefetch=4, **R),
+    "T2_p2": StreamCfg(bx=128, by=8, ty=4, prefetch=2, **R),
+    "T3_z64": StreamCfg(bx=128, by=8, ty=4, prefetch=3, **(R | {"zchunk": 64})),
+    "T4_128x8x2": StreamCfg(bx=128, by=8, ty=2, prefetch=3, **R),
+    "T5_128x16x4": StreamCfg(bx=128, by=16, ty=4, prefetch=3, **R),
+    "T6_64x16x4": StreamCfg(bx=64, by=16, ty=4, prefetch=3, **R),
+    "T7_l2_256": StreamCfg(bx=128, by=8, ty=4, prefetch=3, **(R | {"l2promo": 3})),
+    "T8_192x8x4": StreamCfg(bx=192, by=8, ty=4, prefetch=3, **R),
+    "T9_128x4x4": StreamCfg(bx=128, by=4, ty=4, prefetch=3, **R),
+    "T10_128x12x4": StreamCfg(bx=128, by=12, ty=4, prefetch=3, **R),
+    "T11_nozreg": StreamCfg(bx=128, by=8, ty=4, prefetch=3, **(R | {"zreg": False})),
+    "T12_H2_nonws": StreamCfg(bx=64, by=8, ty=8, prefetch=3, zchunk=128, l2promo=2),
 }
 
 
