@@ -117,9 +117,19 @@ __device__ __forceinline__ void mbar_expect(unsigned long long* b, unsigned byte
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                :: "r"(smem_u32(b)), "r"(bytes) : "memory"); }
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
-               " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-               " @!p bra WAIT_%=;\n}" :: "r"(smem_u32(b)), "r"(parity) : "memory"); }
+  // bounded wait: a pipeline bug must fault (trap -> error at the next sync)
+  // instead of hanging the GPU
+  long long t0 = 0;
+  #pragma unroll 1
+  for (int spin = 0;; ++spin) {
+    unsigned ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    if (ok) return;
+    if (spin == 4096) t0 = clock64();
+    else if (spin > 4096 && (spin & 4095) == 0 && clock64() - t0 > 40000000000LL) __trap();
+  }
+}
 __device__ __forceinline__ void tma_load3(void* dst, const void* tm, int x, int y, int z,
                                           unsigned long long* b) {
   asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -311,10 +321,14 @@ def source_ws(sig: NodeSig, rank: int, cfg: StreamCfg) -> tuple:
     a(f"      const int x0 = bx * {BX}, y0 = by * {BY};")
     a("      const int zs = bzc * (int)p.zc;")
     a("      const int nzl = ((zs + (int)p.zc) < (int)p.nz ? (int)p.zc : (int)p.nz - zs);")
-    maxr = max(s[0][0] for s in slots)
-    a(f"      for (int k = 0; k < nzl + {2 * maxr}; ++k) {{")
+    # Issue planes in the order the consumers NEED them: output z needs plane
+    # k = z + 2*rz of slot s (all of k <= 2*rz at z == 0). Issuing slot by slot
+    # in plain k order would deadlock when a later slot has the larger radius
+    # (the producer would block on an EMPTY slot whose release needs a plane it
+    # has not issued yet).
+    a("      for (int t = 0; t < nzl; ++t) {")
     for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
-        a(f"        if (k < nzl + {2 * rz}) {{")
+        a(f"        for (int k = (t == 0 ? 0 : t + {2 * rz}); k <= t + {2 * rz}; ++k) {{")
         a(f"          const int g = fill{s} + k, stg = g % {stages};")
         a(f"          if (g >= {stages}) mbar_wait(empty{s} + stg, ((g / {stages}) - 1) & 1);")
         a(f"          const int xs = (int)p.cx0[{s}] + x0 - {rx};")

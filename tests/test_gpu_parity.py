@@ -194,3 +194,33 @@ def test_empty_dag():
         job.create_array((8, 8))
         stats = job.run(Dag([], set(), []))
         assert all(s.nodes_executed == 0 for s in stats)
+
+
+@pytest.mark.parametrize("radii", [((0, 0, 0), (2, 1, 1)), ((2, 2, 2), (0, 1, 0)), ((1, 1, 1), (3, 0, 2))])
+def test_stream_multi_slot_mixed_radius(radii):
+    """Two-input 3-D statements whose slots have different z-radii (the TMA
+    producer must issue planes in consumption order, not slot order)."""
+    from paper_2512_19851_b200.ir import add, mul
+    n = 40
+    prog = DagProgram()
+    a = prog.create_array((n, n, n))
+    b = prog.create_array((n, n, n))
+    c = prog.create_array((n, n, n))
+    prog.assign(a, ((3, 30), (5, 33), (2, 37)), cst(1.25))
+    prog.assign(b, ((6, 38), (1, 20), (4, 31)), cst(-0.5))
+    m = 4
+    box = (slice(m, n - m),) * 3
+
+    def shifted(arr, off):
+        return ref(arr, tuple(slice(m + o, n - m + o) for o in off))
+    (ra, rb) = radii
+    expr = add(mul(shifted(a, (-ra[0], ra[1], -ra[2])), shifted(b, (rb[0], -rb[1], rb[2]))),
+               add(shifted(a, (ra[0], -ra[1], ra[2])), shifted(b, (-rb[0], rb[1], -rb[2]))))
+    prog.assign(c, box, expr)
+    want = reference_execute_dag(prog.dag, prog.shapes)
+    job, _ = run_program(prog)
+    try:
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), aid
+    finally:
+        job.close()
