@@ -95,6 +95,7 @@ def migrate_tiles(job, plan: dict) -> dict:
         tile = store.tiles.pop(coords)
         for buf in tile.buffers.values():
             buf.free()
+    store.version += 1  # buffers were added / dropped
     new_map = {c: new for c, (_old, new) in plan.items()}
     job.set_owner_map(new_map)
     for a in sorted(store.arrays):

@@ -130,18 +130,10 @@ class GpuExchangeManager:
         self.buffered: dict = {}
         self.stale_dropped = 0
         self.copy_launches = 0
+        self._geometry: dict = {}  # (array, layout version, owner map) -> boxes
 
-    def _depth(self, array: int):
-        for tile in self.store.tiles.values():
-            return tile.depths[array]
-        return None
-
-    def ensure_round(self, array: int, epoch: int) -> bool:
-        """Start round (array, epoch); returns True (completion is stream-ordered)."""
-        if self.completed.get(array, -1) >= epoch:
-            return True
-        info = self.store.arrays[array]
-        rank = info.rank
+    def _round_geometry(self, array: int, rank: int) -> tuple:
+        """Co-located strip copies and remote (tile, dir, neighbour, owner) list."""
         depth = self._depth(array)
         local_boxes, remote = [], []
         if depth is not None:
@@ -157,6 +149,26 @@ class GpuExchangeManager:
                         local_boxes.append(strip_copy(src, tile.buffers[array], d))
                     else:
                         remote.append((coords, d, nb, owner))
+        return local_boxes, remote
+
+    def _depth(self, array: int):
+        for tile in self.store.tiles.values():
+            return tile.depths[array]
+        return None
+
+    def ensure_round(self, array: int, epoch: int) -> bool:
+        """Start round (array, epoch); returns True (completion is stream-ordered)."""
+        if self.completed.get(array, -1) >= epoch:
+            return True
+        info = self.store.arrays[array]
+        ck = (array, self.store.version, id(self.owner_map))
+        hit = self._geometry.get(ck)
+        if hit is None:
+            hit = self._round_geometry(array, info.rank)
+            if len(self._geometry) > 1024:
+                self._geometry.clear()
+            self._geometry[ck] = hit
+        local_boxes, remote = hit
         if remote:
             if self.transport is None:
                 raise RuntimeError("remote neighbours but no transport configured")

@@ -77,14 +77,25 @@ class GpuExecutor:
         self.transport = None        # peer transport when the job has >1 worker
         self.kernel_events: list = []
         self.graphs = True           # replay repeated batches as CUDA graphs
+        self._analysis: dict = {}    # DAG key -> (metas, plans)
+        self._launches: dict = {}    # (DAG key, node, layout version) -> launches
+        self._recording = None
         self._replay: dict = {}
         self.replays = 0
 
     # -- preparation (executor.py:193-256) ----------------------------------
-    def prepare_batch(self, dag):
+    def prepare_batch(self, dag, key: bytes | None = None):
         shapes = {a: info.shape for a, info in self.store.arrays.items()}
-        metas = analyze_dag(dag, shapes)
-        plans = [compile_plan(n, dag.ast_table) for n in dag.nodes]
+        cached = self._analysis.get(key) if key is not None else None
+        if cached is not None:
+            metas, plans = cached
+        else:
+            metas = analyze_dag(dag, shapes)
+            plans = [compile_plan(n, dag.ast_table) for n in dag.nodes]
+            if key is not None:
+                if len(self._analysis) > 256:
+                    self._analysis.clear()
+                self._analysis[key] = (metas, plans)
         for node in dag.nodes:
             if len(node.statements) > 1 and node_hazard(node):
                 raise MalformedDag(f"node {node.node_id} has dependent statements")
@@ -143,7 +154,7 @@ class GpuExecutor:
         CUDA graph instead of being re-analysed and re-launched node by node;
         the epoch / round bookkeeping is applied exactly as a fresh run would."""
         if key is None or not self.graphs or self.transport is not None or self.time_kernels:
-            return self._execute(dag)
+            return self._execute(dag, key)
         sig = (key, self._state_sig())
         ent = self._replay.get(sig)
         if ent is not None and ent.get("graph") is not None:
@@ -155,7 +166,7 @@ class GpuExecutor:
             launches0 = self.dev.launches
             self.dev.graph_begin(COMPUTE)
             try:
-                stats = self._execute(dag)
+                stats = self._execute(dag, key)
             except BaseException:
                 try:
                     self.dev.graph_end(COMPUTE).close()
@@ -168,7 +179,7 @@ class GpuExecutor:
             graph.launch(COMPUTE)
             ent["graph"] = graph
         else:
-            stats = self._execute(dag)
+            stats = self._execute(dag, key)
         after = self._epoch_snapshot()
         if self._state_sig()[0] != sig[1][0]:
             return stats  # buffers were reallocated: not a steady-state batch
@@ -227,11 +238,11 @@ class GpuExecutor:
         self._replay.clear()
 
     # -- execution (executor.py:258-348) ------------------------------------
-    def _execute(self, dag) -> BatchStats:
+    def _execute(self, dag, key: bytes | None = None) -> BatchStats:
         t0 = time.perf_counter()
         before = self.exchanges.snapshot_stats()
         launches0 = self.dev.launches
-        metas, plans, pushes = self.prepare_batch(dag)
+        metas, plans, pushes = self.prepare_batch(dag, key)
         stats = BatchStats(prepare_ms=(time.perf_counter() - t0) * 1e3)
         for a, e in pushes.get(None, ()):
             self.exchanges.ensure_round(a, e)
@@ -247,7 +258,7 @@ class GpuExecutor:
             if self.transport is not None:
                 for a in sorted(node.writes):
                     self.transport.before_write(a)
-            self.launch_node(node, plans[node.node_id])
+            self.launch_node(node, plans[node.node_id], key)
             stats.kernel_launches += len(self.store.tiles)
             stats.compute_ms += (time.perf_counter() - t_node) * 1e3
             for a in sorted(node.writes):
@@ -293,15 +304,7 @@ class GpuExecutor:
             cz.append(z + dz)
         it.update(cx0=cx, cy0=cy, cz0=cz)
         params = stream.pack_params(it, tmaps, len(ps.inputs))
-        grid = (it["blocks"], 1, 1)
-        if self.time_kernels:
-            ev0, ev1 = self.dev.event(), self.dev.event()
-            ev0.record(COMPUTE)
-            self.dev.launch(kern, grid, params, COMPUTE)
-            ev1.record(COMPUTE)
-            self.kernel_events.append((ev0, ev1))
-        else:
-            self.dev.launch(kern, grid, params, COMPUTE)
+        self._launch(kern, (it["blocks"], 1, 1), params)
 
     def _boxes(self, plan):
         """(statement index, tile, box lo (local), box extent) for non-empty intersections."""
@@ -324,7 +327,36 @@ class GpuExecutor:
                     out.append((si, ps, tile, tuple(lo), tuple(n)))
         return out
 
-    def launch_node(self, node, plan) -> None:
+    def launch_node(self, node, plan, key: bytes | None = None) -> None:
+        ck = (key, node.node_id, self.store.version) if key is not None else None
+        recorded = self._launches.get(ck) if ck is not None else None
+        if recorded is not None and not self.time_kernels:
+            for kern, grid, params in recorded:
+                self.dev.launch(kern, grid, params, COMPUTE)
+            return
+        self._recording = [] if ck is not None else None
+        try:
+            self._launch_node(node, plan)
+        finally:
+            rec, self._recording = self._recording, None
+        if ck is not None and rec is not None:
+            if len(self._launches) > 8192:
+                self._launches.clear()
+            self._launches[ck] = rec
+
+    def _launch(self, kern, grid, params) -> None:
+        if self._recording is not None:
+            self._recording.append((kern, grid, params))
+        if self.time_kernels:
+            ev0, ev1 = self.dev.event(), self.dev.event()
+            ev0.record(COMPUTE)
+            self.dev.launch(kern, grid, params, COMPUTE)
+            ev1.record(COMPUTE)
+            self.kernel_events.append((ev0, ev1))
+        else:
+            self.dev.launch(kern, grid, params, COMPUTE)
+
+    def _launch_node(self, node, plan) -> None:
         boxes = self._boxes(plan)
         if not boxes:
             return
@@ -368,11 +400,4 @@ class GpuExecutor:
                 it["blk0"] = blk
                 blk += it["bxn"] * it["byn"] * it["nzb"]
             params = codegen.pack_items(chunk, sig.max_in, n_items)
-            if self.time_kernels:
-                ev0, ev1 = self.dev.event(), self.dev.event()
-                ev0.record(COMPUTE)
-                self.dev.launch(kern, (blk, 1, 1), params, COMPUTE)
-                ev1.record(COMPUTE)
-                self.kernel_events.append((ev0, ev1))
-            else:
-                self.dev.launch(kern, (blk, 1, 1), params, COMPUTE)
+            self._launch(kern, (blk, 1, 1), params)

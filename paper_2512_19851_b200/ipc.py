@@ -75,6 +75,8 @@ class IpcPeerTransport(LocalPeerTransport):
         self.peer_maps: dict = {}      # (owner, coords, array) -> (layout TileBuffer, addr)
         self.opened: list = []
         self.spin_s = 0.0
+        self.peer_version = 0
+        self._pulls: dict = {}
 
     # -- handle exchange ---------------------------------------------------------
     def event_handles(self) -> dict:
@@ -98,6 +100,7 @@ class IpcPeerTransport(LocalPeerTransport):
 
     def open_peer_buffers(self, tables: list) -> None:
         self.close_peer_buffers()
+        self.peer_version += 1
         for owner, table in enumerate(tables):
             if owner == self.w:
                 continue
@@ -272,18 +275,21 @@ class IpcGpuJob:
         return aid
 
     def run_bytes(self, blob: bytes) -> list:
+        import hashlib
+
         from .wire import decode_dag
 
-        dag = self._decoded.get(blob)
+        key = hashlib.blake2b(blob, digest_size=16).digest()
+        dag = self._decoded.get(key)
         if dag is None:
-            dag = self._decoded[blob] = decode_dag(blob)
             if len(self._decoded) > 64:
                 self._decoded.clear()
-        return self.run(dag)
+            dag = self._decoded[key] = decode_dag(blob)
+        return self.run(dag, key)
 
     def run(self, dag, key: bytes | None = None) -> list:
         try:
-            return [self.executor.execute_batch(dag)]
+            return [self.executor.execute_batch(dag, key)]
         except BaseException as exc:
             if self.transport is not None:
                 self.transport.abort(exc)
