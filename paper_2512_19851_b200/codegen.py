@@ -252,7 +252,7 @@ def kernel_source_for(plan, rank: int, dtype: int, skeleton: str = "auto") -> tu
     """
     from . import stream
 
-    key = (tuple(p.instructions for p in plan.statements), rank, dtype, skeleton, stream.DEFAULT)
+    key = (tuple(p.instructions for p in plan.statements), rank, dtype, skeleton, stream.cfg_for(rank))
     hit = _SRC_CACHE.get(key)
     if hit is not None:
         return hit

@@ -68,6 +68,11 @@ def _env_cfg() -> StreamCfg:
 
 
 DEFAULT = _env_cfg()
+DEFAULT_2D = StreamCfg(bx=int(os.environ.get("EST_STREAM2D_BX", 128)),
+                       by=int(os.environ.get("EST_STREAM2D_BY", 16)),
+                       ty=int(os.environ.get("EST_STREAM2D_TY", 4)),
+                       prefetch=int(os.environ.get("EST_STREAM2D_PREFETCH", 3)),
+                       persistent=True, ws=True, zreg=False, l2promo=2)
 
 
 def layout(st: StmtSig, dtype: int, cfg: StreamCfg):
@@ -88,9 +93,19 @@ def layout(st: StmtSig, dtype: int, cfg: StreamCfg):
     return slots, off, off + 8 * n_bars + 1024
 
 
+def cfg_for(rank: int) -> StreamCfg:
+    """Rank-3 nodes stream along z; rank-2 nodes run the same warp-specialised
+    TMA pipeline on a (1, Y, X) view: every item is one (BY+2ry) x (BX+2rx)
+    tile, and the persistent grid lets the producer prefetch the NEXT items'
+    tiles while the current one is computed."""
+    return DEFAULT if rank == 3 else DEFAULT_2D
+
+
 def eligible(stmts, rank: int, dtype: int = DTYPE_F64, cfg: StreamCfg | None = None) -> bool:
-    cfg = cfg or DEFAULT
-    if rank != 3 or len(stmts) != 1 or stmts[0].arity == 0:
+    cfg = cfg or cfg_for(rank)
+    if rank not in (2, 3) or len(stmts) != 1 or stmts[0].arity == 0:
+        return False
+    if rank == 2 and not cfg.ws:
         return False
     rad = slot_radius(stmts[0]).values()
     if any(max(r) > MAX_RADIUS for r in rad):
@@ -140,7 +155,7 @@ __device__ __forceinline__ void tma_load3(void* dst, const void* tm, int x, int 
 
 
 def source(sig: NodeSig, rank: int, cfg: StreamCfg | None = None) -> tuple:
-    cfg = cfg or DEFAULT
+    cfg = cfg or cfg_for(rank)
     if cfg.ws:
         return source_ws(sig, rank, cfg)
     BX, BY, TY = cfg.bx, cfg.by, cfg.ty
@@ -456,6 +471,12 @@ def item_geometry(item: dict, sm_count: int, geom: dict) -> None:
         item["zc"] = -(-item["nz"] // nzc)
     else:
         item["zc"] = min(cfg.zchunk, item["nz"])
+        cap = sm_count * blocks_per_sm(geom["smem"], cfg)
+        if n_xy * -(-item["nz"] // item["zc"]) < 4 * cap:
+            # thin slab (e.g. 1024^3 split over 8 GPUs): split z finer so the
+            # grid is several waves deep, balancing the last wave
+            nzc = _choose_zchunks(item["nz"], n_xy, cap)
+            item["zc"] = -(-item["nz"] // nzc)
     item["nzc"] = -(-item["nz"] // item["zc"])
     n_items = n_xy * item["nzc"]
     item["blocks"] = min(n_items, sm_count * blocks_per_sm(geom["smem"], cfg)) if cfg.persistent else n_items
