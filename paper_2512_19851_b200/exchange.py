@@ -131,6 +131,7 @@ class GpuExchangeManager:
         self.stale_dropped = 0
         self.copy_launches = 0
         self._geometry: dict = {}  # (array, layout version, owner map) -> boxes
+        self.pending: dict = {}    # array -> posted-but-unpulled round token
 
     def _round_geometry(self, array: int, rank: int) -> tuple:
         """Co-located strip copies and remote (tile, dir, neighbour, owner) list."""
@@ -156,10 +157,26 @@ class GpuExchangeManager:
             return tile.depths[array]
         return None
 
-    def ensure_round(self, array: int, epoch: int) -> bool:
-        """Start round (array, epoch); returns True (completion is stream-ordered)."""
+    def finish_pending(self, array: int | None = None, overlap: bool = False) -> list:
+        """Enqueue deferred peer pulls (all, or one array's); returns their round ids."""
+        done = []
+        for a in ([array] if array is not None else sorted(self.pending)):
+            token = self.pending.pop(a, None)
+            if token is not None:
+                self.transport.finish(token, overlap=overlap)
+                done.append(token[1])
+        return done
+
+    def ensure_round(self, array: int, epoch: int, defer: bool = False) -> bool:
+        """Start round (array, epoch); returns True (completion is stream-ordered).
+
+        With `defer` (multi-worker, push-plan rounds) the peer pull is posted
+        but not enqueued; the executor finishes it right before / overlapped
+        with the next node that reads the array (`finish_pending`)."""
         if self.completed.get(array, -1) >= epoch:
             return True
+        if self.pending:
+            self.finish_pending()  # keep at most one round in flight on the host
         info = self.store.arrays[array]
         ck = (array, self.store.version, id(self.owner_map))
         hit = self._geometry.get(ck)
@@ -176,7 +193,10 @@ class GpuExchangeManager:
         if self.transport is not None:
             # every worker takes part in every round, owning tiles or not, so the
             # transport's per-round sequencing stays globally aligned
-            self.transport.exchange(array, epoch, remote, local_boxes)
+            if defer:
+                self.pending[array] = self.transport.post(array, epoch, remote, local_boxes)
+            else:
+                self.transport.exchange(array, epoch, remote, local_boxes)
         elif local_boxes:
             self.store.dev.copy_boxes(local_boxes, ELEM[info.dtype])
             self.copy_launches += 1

@@ -77,6 +77,7 @@ class GpuExecutor:
         self.transport = None        # peer transport when the job has >1 worker
         self.kernel_events: list = []
         self.graphs = True           # replay repeated batches as CUDA graphs
+        self.overlap = True          # defer push-plan peer pulls behind interior planes
         self._analysis: dict = {}    # DAG key -> (metas, plans)
         self._launches: dict = {}    # (DAG key, node, layout version) -> launches
         self._recording = None
@@ -255,18 +256,33 @@ class GpuExecutor:
                 if target and self.exchanges.ghost_generation(a) != target:
                     self.exchanges.ensure_round(a, target)
             t_node = time.perf_counter()
+            plan = plans[node.node_id]
             if self.transport is not None:
                 for a in sorted(node.writes):
                     self.transport.before_write(a)
-            self.launch_node(node, plans[node.node_id], key)
+            pending = self.exchanges.pending
+            if pending and set(pending) & set(meta.array_max_offset) and self.overlap_eligible(plan):
+                # halo/compute overlap: planes that read no ghost cells go first,
+                # the deferred peer pull runs on the copy lane meanwhile, the
+                # ghost-touching planes run after the compute lane joins it
+                self.launch_node(node, plan, key, "interior")
+                for r in self.exchanges.finish_pending(overlap=True):
+                    self.transport.join_copy(r)
+                self.launch_node(node, plan, key, "boundary")
+            else:
+                if pending:
+                    self.exchanges.finish_pending()
+                self.launch_node(node, plan, key)
             stats.kernel_launches += len(self.store.tiles)
             stats.compute_ms += (time.perf_counter() - t_node) * 1e3
             for a in sorted(node.writes):
                 self.store.bump_local_epoch(a)
             for a, e in pushes.get(node.node_id, ()):
-                self.exchanges.ensure_round(a, e)
+                self.exchanges.ensure_round(a, e, defer=self.overlap and self.transport is not None)
             stats.nodes_executed += 1
             stats.node_ms[node.node_id] = (time.perf_counter() - t_node) * 1e3
+        if self.exchanges.pending:
+            self.exchanges.finish_pending()
         after = self.exchanges.snapshot_stats()
         for a, n in after["rounds"].items():
             d = n - before["rounds"].get(a, 0)
@@ -327,8 +343,8 @@ class GpuExecutor:
                     out.append((si, ps, tile, tuple(lo), tuple(n)))
         return out
 
-    def launch_node(self, node, plan, key: bytes | None = None) -> None:
-        ck = (key, node.node_id, self.store.version) if key is not None else None
+    def launch_node(self, node, plan, key: bytes | None = None, zsplit: str | None = None) -> None:
+        ck = (key, node.node_id, self.store.version, zsplit) if key is not None else None
         recorded = self._launches.get(ck) if ck is not None else None
         if recorded is not None and not self.time_kernels:
             for kern, grid, params in recorded:
@@ -336,7 +352,7 @@ class GpuExecutor:
             return
         self._recording = [] if ck is not None else None
         try:
-            self._launch_node(node, plan)
+            self._launch_node(node, plan, zsplit)
         finally:
             rec, self._recording = self._recording, None
         if ck is not None and rec is not None:
@@ -356,7 +372,31 @@ class GpuExecutor:
         else:
             self.dev.launch(kern, grid, params, COMPUTE)
 
-    def _launch_node(self, node, plan) -> None:
+    def _zranges(self, zsplit, geom, rank: int, tile, ps, local, nz: int) -> list:
+        """Output-plane ranges to launch: all, or the part that reads only
+        interior planes ("interior") / the part that touches ghost planes."""
+        if zsplit is None or rank != 3:
+            return [(0, nz)]
+        rz = max(s[0][0] for s in geom["slots"])
+        ez = tile.buffers[ps.output].ext[0]
+        lo = min(nz, max(0, rz - local[0]))
+        hi = max(lo, min(nz, ez - rz - local[0]))
+        if zsplit == "interior":
+            return [(lo, hi)] if hi > lo else []
+        if hi <= lo:
+            return [(0, nz)]
+        return [r for r in ((0, lo), (hi, nz)) if r[1] > r[0]]
+
+    def overlap_eligible(self, plan) -> bool:
+        """Halo/compute overlap applies to single-tile rank-3 stream nodes."""
+        if len(self.store.tiles) != 1 or len(plan.statements) != 1:
+            return False
+        info = self.store.arrays[plan.statements[0].output]
+        if info.rank != 3:
+            return False
+        return codegen.kernel_source_for(plan, 3, info.dtype, self.skeleton)[6].skeleton == "stream"
+
+    def _launch_node(self, node, plan, zsplit=None) -> None:
         boxes = self._boxes(plan)
         if not boxes:
             return
@@ -381,9 +421,14 @@ class GpuExecutor:
                 it["ipy"].append(ib.py)
                 it["ipz"].append(ib.pz)
             if sig.skeleton == "stream":
-                stream.item_geometry(it, self.dev.sm_count, geom)
-                self._launch_stream(kern, sig, geom, it, tile, ps, [
-                    [g - o for g, o in zip(g_lo, self.store.decomp.tile_origin(shape, tile.coords))]])
+                local = [g - o for g, o in zip(g_lo, self.store.decomp.tile_origin(shape, tile.coords))]
+                for z_a, z_b in self._zranges(zsplit, geom, rank, tile, ps, local, n3[0]):
+                    sub = dict(it, out=it["out"] + z_a * out_buf.pz * out_buf.elem, nz=z_b - z_a)
+                    sub_local = list(local)
+                    if rank == 3:
+                        sub_local[0] += z_a
+                    stream.item_geometry(sub, self.dev.sm_count, geom)
+                    self._launch_stream(kern, sig, geom, sub, tile, ps, [sub_local])
                 continue
             else:
                 bx, by, _ = block

@@ -32,7 +32,7 @@ from __future__ import annotations
 import threading
 
 from .codegen import ELEM
-from .device import COMPUTE
+from .device import COMPUTE, COPY
 from .exchange import strip_copy
 
 RING = 16
@@ -123,6 +123,12 @@ class LocalPeerTransport:
 
     # -- protocol -------------------------------------------------------------
     def exchange(self, array: int, epoch: int, remote, local_boxes) -> None:
+        self.finish(self.post(array, epoch, remote, local_boxes), overlap=False)
+
+    def post(self, array: int, epoch: int, remote, local_boxes):
+        """Steps 1-2: READY record + co-located copies; the peer pull is left
+        to `finish`, which the executor may defer past the next node's
+        interior launch (halo/compute overlap)."""
         r = self.seq
         self.seq += 1
         slot = r % RING
@@ -131,10 +137,23 @@ class LocalPeerTransport:
         self.publish("ready", r)
         if local_boxes:
             self.dev.copy_boxes(local_boxes, elem)
+        return (array, r, remote, elem)
+
+    def finish(self, token, overlap: bool = False) -> None:
+        """Steps 3-4. With `overlap` the pull runs on the COPY stream (after
+        this worker's own READY, so the previous readers of the ghost are
+        done) and the compute stream only joins it before the boundary work
+        (`join_copy`)."""
+        array, r, remote, elem = token
+        slot = r % RING
+        lane = COMPUTE
+        if overlap and remote:
+            lane = COPY
+            self.ready[slot].wait(COPY)
         peers = sorted({owner for _, _, _, owner in remote})
         for p in peers:
             self.wait_seq(p, "ready", r)
-            self.peer_event(p, "ready", slot).wait(COMPUTE)
+            self.peer_event(p, "ready", slot).wait(lane)
         if remote:
             ck = (array, self.store.version, self.peer_version, id(remote))
             boxes = self._pulls.get(ck)
@@ -147,12 +166,16 @@ class LocalPeerTransport:
                 if len(self._pulls) > 1024:
                     self._pulls.clear()
                 self._pulls[ck] = boxes
-            self.dev.copy_boxes(boxes, elem)
+            self.dev.copy_boxes(boxes, elem, lane)
             self.pull_launches += 1
-        self.pulled[slot].record(COMPUTE)
+        self.pulled[slot].record(lane)
         self.publish("pulled", r)
         if peers:
             self.readers[array] = (r, peers)
+
+    def join_copy(self, r: int) -> None:
+        """Compute stream waits for the overlapped pull of round r."""
+        self.pulled[r % RING].wait(COMPUTE)
 
     def before_write(self, array: int) -> None:
         ent = self.readers.pop(array, None)

@@ -55,6 +55,7 @@ class FakeDevice:
         self._next = 1 << 40
         self.allocated: dict = {}
         self.opened: list = []
+        self.lane_copies: dict = {}
 
     def alloc(self, n):
         p = self._next
@@ -73,6 +74,7 @@ class FakeDevice:
 
     def copy_boxes(self, boxes, elem, stream=0):
         self.launches += 1
+        self.lane_copies[stream] = self.lane_copies.get(stream, 0) + 1
         for b in boxes:
             self.copies.append(("strip", b.src, b.dst, b.nx, b.ny, b.nz))
 

@@ -54,6 +54,7 @@ def host_logic_rank(rank, world, kind, odf, batch):
     out = {"rounds": rounds, "net": sum(s.net_messages for s in stats),
            "launches": sum(s.kernel_launches for s in stats),
            "strips": len(strips), "seq": job.transport.seq,
+           "copy_lane_pulls": job.dev.lane_copies.get(1, 0),
            "tiles": sorted(job.store.tiles)}
     job.close()
     return out
