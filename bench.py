@@ -73,6 +73,20 @@ def bytes_per_iter(w) -> int:
     return 8 * (m * m + 4 * m + m * m)
 
 
+def bytes_per_launch(w, tag) -> int:
+    """Algorithmic HBM bytes of one launch of kernel kind `tag` = (kind, sweeps).
+
+    A plain node kernel is one sweep (bytes_per_iter). A temporal chain of K
+    sweeps (temporal.py) reads the input array once and writes each of the two
+    arrays once: elem * (N_in + 2 * N_out)."""
+    kind, sweeps = tag
+    if kind != "tb":
+        return bytes_per_iter(w)
+    n = w["n"]
+    m = n - 2
+    return 8 * ((m ** 3 + 6 * m ** 2) + 2 * m ** 3)
+
+
 def load_peaks() -> tuple:
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -323,11 +337,16 @@ def main():
         for _ in range(2):
             one_step()
         job.sync()
-    kt = [a.elapsed_ms(b) for a, b in ex.kernel_events]
+    by_tag: dict = {}
+    for a, b, tag in ex.kernel_events:
+        by_tag.setdefault(tag, []).append(a.elapsed_ms(b))
     ex.time_kernels = False
-    for a, b in ex.kernel_events:
+    for a, b, _tag in ex.kernel_events:
         a.close(), b.close()
     ex.kernel_events.clear()
+    # dominant kernel = the kind with the largest total device time
+    dom = max(by_tag, key=lambda t: sum(by_tag[t])) if by_tag else ("node", 1)
+    kt = by_tag.get(dom, [])
     if dist:
         import torch
         t = torch.tensor([dev_ms], dtype=torch.float64)
@@ -360,14 +379,18 @@ def main():
 
     # ---- roofline ------------------------------------------------------------
     peak, peak_src = load_peaks()
+    sweeps = dom[1]
     mean_k = statistics.mean(kt) if kt else dev_ms / max(1, args.steps * w["iters_per_step"])
-    bytes_launch = bytes_per_iter(w) // world if world > 1 else bytes_per_iter(w)
+    bytes_launch = bytes_per_launch(w, dom)
+    if world > 1:
+        bytes_launch //= world
     achieved = bytes_launch / (mean_k / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(args.workload, {}).get("dram_bytes_per_launch")
+            pkey = args.workload + ("_tb%d" % sweeps if dom[0] == "tb" else "")
+            traffic = json.load(open(prof)).get(pkey, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -385,6 +408,8 @@ def main():
                    "kernel_timing": "inline" if inline_timing else "separate 2-step pass (graphs in timed region)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "est_tb (K=%d fused sweeps)" % sweeps if dom[0] == "tb" else "est_stream/est_node (1 sweep)",
+                     "sweeps_per_launch": sweeps,
                      "kernel_ms": mean_k, "bytes_per_launch": bytes_launch,
                      "peak_source": peak_src,
                      "frac_of_8TBs": achieved / 8000.0},

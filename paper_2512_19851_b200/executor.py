@@ -26,7 +26,7 @@ from __future__ import annotations
 import time
 from dataclasses import dataclass, field
 
-from . import codegen, stream
+from . import codegen, stream, temporal
 from .analysis import analyze_dag, compile_plan
 from .device import COMPUTE
 from .errors import MalformedDag
@@ -83,6 +83,10 @@ class GpuExecutor:
         self._recording = None
         self._replay: dict = {}
         self.replays = 0
+        self.temporal = temporal.ENABLED  # fuse ping-pong sweep chains (temporal.py)
+        self.tb_cfg = temporal.DEFAULT
+        self._scratch: dict = {}     # array -> twin TileBuffer for temporal chains
+        self._tb_sched: dict = {}
 
     # -- preparation (executor.py:193-256) ----------------------------------
     def prepare_batch(self, dag, key: bytes | None = None):
@@ -237,6 +241,7 @@ class GpuExecutor:
             if ent.get("graph") is not None:
                 ent["graph"].close()
         self._replay.clear()
+        self.release_scratch()
 
     # -- execution (executor.py:258-348) ------------------------------------
     def _execute(self, dag, key: bytes | None = None) -> BatchStats:
@@ -245,6 +250,7 @@ class GpuExecutor:
         launches0 = self.dev.launches
         metas, plans, pushes = self.prepare_batch(dag, key)
         stats = BatchStats(prepare_ms=(time.perf_counter() - t0) * 1e3)
+        tb = self.temporal_schedule(dag, plans, key)
         for a, e in pushes.get(None, ()):
             self.exchanges.ensure_round(a, e)
         for node in dag.nodes:
@@ -261,7 +267,14 @@ class GpuExecutor:
                 for a in sorted(node.writes):
                     self.transport.before_write(a)
             pending = self.exchanges.pending
-            if pending and set(pending) & set(meta.array_max_offset) and self.overlap_eligible(plan):
+            chain = tb.get(node.node_id)
+            if chain is not None:
+                # temporal chain: its lead node launches the fused K-sweep
+                # kernel; members only keep the per-node bookkeeping (a single
+                # tile without transport has no device work between sweeps)
+                if chain[0] == "lead":
+                    self._launch_tb(node, plan, chain[1], key)
+            elif pending and set(pending) & set(meta.array_max_offset) and self.overlap_eligible(plan):
                 # halo/compute overlap: planes that read no ghost cells go first,
                 # the deferred peer pull runs on the copy lane meanwhile, the
                 # ghost-touching planes run after the compute lane joins it
@@ -292,6 +305,119 @@ class GpuExecutor:
         stats.gpu_launches = self.dev.launches - launches0
         stats.wall_ms = (time.perf_counter() - t0) * 1e3
         return stats
+
+    # -- temporal blocking (temporal.py) ----------------
+    def _tb_candidate(self, plan):
+        if len(plan.statements) != 1:
+            return None
+        ps = plan.statements[0]
+        if len(ps.inputs) != 1:
+            return None
+        a, b = ps.inputs[0], ps.output
+        ia, ib = self.store.arrays.get(a), self.store.arrays.get(b)
+        if ia is None or ib is None or ia.rank != 3 or ia.shape != ib.shape or ia.dtype != ib.dtype:
+            return None
+        tile = next(iter(self.store.tiles.values()))
+        ba, bb = tile.buffers[a], tile.buffers[b]
+        if (ba.depth, ba.py, ba.pz, ba.xoff) != (bb.depth, bb.py, bb.pz, bb.xoff):
+            return None
+        sig = codegen.stmt_sig(ps, 3)
+        if not temporal.eligible(sig, ia.dtype, self.tb_cfg):
+            return None
+        return (a, b, tuple(ps.output_slice_bounds), ps.instructions)
+
+    def temporal_schedule(self, dag, plans, key=None) -> dict:
+        """node id -> ("lead", chain index in its run) | ("member",).
+
+        Runs of consecutive candidate nodes that ping-pong A -> B -> A with the
+        same statement and output slice are cut into chains of K nodes; the
+        number of chains per run is kept even so A ends in its own buffer.
+        Only for one tile per job without transport (no exchange between
+        sweeps); everything else runs node by node."""
+        if (not self.temporal or self.transport is not None or len(self.store.tiles) != 1
+                or self.store.decomp.n_tiles != 1 or self.skeleton not in ("auto", "tb")):
+            return {}
+        ck = (key, self.store.version, self.tb_cfg) if key is not None else None
+        hit = self._tb_sched.get(ck) if ck is not None else None
+        if hit is not None:
+            return hit
+        K = self.tb_cfg.k
+        cand = [self._tb_candidate(p) for p in plans]
+        sched: dict = {}
+        i, n = 0, len(cand)
+        while i < n:
+            c = cand[i]
+            if c is None:
+                i += 1
+                continue
+            j = i + 1
+            while (j < n and cand[j] is not None and cand[j][2:] == c[2:]
+                   and cand[j][0] == cand[j - 1][1] and cand[j][1] == cand[j - 1][0]):
+                j += 1
+            m = (j - i) // K
+            m -= m % 2
+            for ch in range(m):
+                lead = i + ch * K
+                sched[dag.nodes[lead].node_id] = ("lead", ch)
+                for q in range(1, K):
+                    sched[dag.nodes[lead + q].node_id] = ("member",)
+            i = j
+        if ck is not None:
+            if len(self._tb_sched) > 256:
+                self._tb_sched.clear()
+            self._tb_sched[ck] = sched
+        return sched
+
+    def _scratch_for(self, array: int, buf):
+        tw = self._scratch.get(array)
+        if tw is not None and (tw.ext, tw.depth, tw.dtype, tw.nbytes) == (buf.ext, buf.depth, buf.dtype, buf.nbytes):
+            return tw
+        if tw is not None:
+            tw.free()
+        from .tiles import TileBuffer
+        tw = TileBuffer(self.dev, buf.ext[3 - buf.rank:], buf.depth[3 - buf.rank:], buf.dtype)
+        self._scratch[array] = tw
+        return tw
+
+    def release_scratch(self) -> None:
+        for tw in self._scratch.values():
+            tw.free()
+        self._scratch.clear()
+
+    def _launch_tb(self, node, plan, ch: int, key) -> None:
+        ps = plan.statements[0]
+        a, b = ps.inputs[0], ps.output
+        tile = next(iter(self.store.tiles.values()))
+        home, bbuf = tile.buffers[a], tile.buffers[b]
+        twin = self._scratch_for(a, home)
+        d = home.depth
+        s_lo = tuple(lo + dd for (lo, _), dd in zip(ps.output_slice_bounds, d))
+        s_hi = tuple(hi + dd for (_, hi), dd in zip(ps.output_slice_bounds, d))
+        if ch == 0:
+            # the twin must hold A's values outside S (never written by a chain)
+            self.dev.copy_boxes(temporal.complement_boxes(home, home.ptr, twin.ptr, s_lo, s_hi), home.elem)
+        ck = (key, node.node_id, self.store.version, "tb") if key is not None else None
+        rec = self._launches.get(ck) if ck is not None else None
+        if rec is not None and not self.time_kernels:
+            for kern, grid, params in rec:
+                self.dev.launch(kern, grid, params, COMPUTE)
+            return
+        src_buf, dst_buf = (home, twin) if ch % 2 == 0 else (twin, home)
+        sig = codegen.stmt_sig(ps, 3)
+        src, name, block, smem, lay = temporal.source(sig, self.store.arrays[a].dtype, self.tb_cfg)
+        kern = self.dev.kernel(src, name, block, smem)
+        geo = temporal.item_geometry(s_lo, s_hi, self.dev.sm_count, lay)
+        tm = self._tmap(src_buf, (lay["w0"], lay["h0"], 1), self.tb_cfg.l2promo)
+        org = home.xoff * home.elem
+        params = temporal.pack_params(tm, src_buf.ptr + org, bbuf.ptr + org, dst_buf.ptr + org,
+                                      home, s_lo, s_hi, geo)
+        self._recording = [] if ck is not None else None
+        try:
+            self._launch(kern, (geo["blocks"], 1, 1), params, tag=("tb", self.tb_cfg.k))
+        finally:
+            rec, self._recording = self._recording, None
+        if ck is not None and rec is not None:
+            self._launches[ck] = rec
 
     # -- node -> kernel launch ----------------------------------------------
     def _tmap(self, buf, box, l2promo: int = 3) -> bytes:
@@ -360,7 +486,8 @@ class GpuExecutor:
                 self._launches.clear()
             self._launches[ck] = rec
 
-    def _launch(self, kern, grid, params) -> None:
+    def _launch(self, kern, grid, params, tag=("node", 1)) -> None:
+        """`tag` = (kernel kind, sweeps covered) for the timing records."""
         if self._recording is not None:
             self._recording.append((kern, grid, params))
         if self.time_kernels:
@@ -368,7 +495,7 @@ class GpuExecutor:
             ev0.record(COMPUTE)
             self.dev.launch(kern, grid, params, COMPUTE)
             ev1.record(COMPUTE)
-            self.kernel_events.append((ev0, ev1))
+            self.kernel_events.append((ev0, ev1, tag))
         else:
             self.dev.launch(kern, grid, params, COMPUTE)
 

@@ -1,0 +1,367 @@
+"""The "tb" skeleton: temporal blocking of K consecutive ping-pong sweeps.
+
+A batch of heat/Jacobi iterations is a chain of single-statement rank-3 nodes
+`B[S] = f(A[S + offsets]); A[S] = f(B[S + offsets]); ...` (
+reference semantics executor.py:258-348: nodes run in order, statement at a
+time). On one GPU with one tile no halo exchange happens between them, so K of
+them (K even) can run as ONE kernel that reads A once from HBM, keeps the
+intermediate sweeps in shared memory and writes only the arrays' final values:
+24 B per K updates instead of 16 B per update (12 B/LUP at K = 2).
+
+Every point is still computed by the same generated expression
+(codegen._emit_expr: one correctly rounded IEEE op per plan instruction, no
+contraction), so results are bit-identical to K separate sweeps. Epochs,
+rounds and launch counts are kept per node by the executor.
+
+Kernel structure (warp-specialised like stream.source_ws):
+* work item = a BX x BY output column of S over ZC planes; step j (1..K) of
+  the chain covers the item tile expanded by (K-j)*r in y/x (overlapped
+  tiling) and trails step j-1 by rz planes in z;
+* producer warp: one TMA (`cp.async.bulk.tensor.3d`) per input plane of A
+  (tile + K*r halo) into an mbarrier-gated ring (full/empty barriers);
+* compute warps, per input plane: step 1 reads the TMA ring, step j > 1 reads
+  step j-1's shared-memory plane ring (2rz+2 planes); one named barrier
+  between steps. Cells of a step's region outside S keep the array's stored
+  value (read from its home buffer; S's complement is never written);
+* stores: step K-1 (array B, final) in place inside S; step K (array A,
+  final) into A's *other* home buffer, because neighbouring CTAs still read A
+  through TMA. The executor alternates A between its tile buffer and a
+  scratch twin (chains come in pairs, so A ends in its own buffer) and copies
+  S's complement into the twin at the start of each run.
+"""
+
+from __future__ import annotations
+
+import os
+import struct
+from dataclasses import dataclass
+
+from .codegen import CTYPE, ELEM, StmtSig, _emit_expr, slot_radius
+from .stream import _PTX_HELPERS
+
+MAX_RADIUS = 2
+SMEM_BUDGET = 200 * 1024
+SMEM_PER_SM = 228 * 1024
+
+
+@dataclass(frozen=True)
+class TbCfg:
+    k: int = 2              # sweeps per launch (even)
+    bx: int = 64            # output columns per item
+    by: int = 16            # output rows per item
+    rpt: int = 2            # rows of the step-1 region per compute thread
+    prefetch: int = 2       # input planes in flight beyond the z window
+    zchunk: int = 128       # planes per item
+    l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
+    persistent: bool = False
+
+
+def _env_cfg() -> TbCfg:
+    e = os.environ.get
+    d = TbCfg()
+    return TbCfg(k=int(e("EST_TB_K", d.k)), bx=int(e("EST_TB_BX", d.bx)), by=int(e("EST_TB_BY", d.by)),
+                 rpt=int(e("EST_TB_RPT", d.rpt)), prefetch=int(e("EST_TB_PREFETCH", d.prefetch)),
+                 zchunk=int(e("EST_TB_ZCHUNK", d.zchunk)), l2promo=int(e("EST_TB_L2PROMO", d.l2promo)),
+                 persistent=e("EST_TB_PERSISTENT", "0") == "1")
+
+
+DEFAULT = _env_cfg()
+ENABLED = os.environ.get("EST_TB", "0") == "1"
+
+
+def _round(v: int, m: int) -> int:
+    return -(-v // m) * m
+
+
+def z_star(st: StmtSig) -> bool:
+    """Every load off the centre plane is a pure z offset (dz, 0, 0)."""
+    return all(i[2][0] == 0 or (i[2][1] == 0 and i[2][2] == 0) for i in st.instructions if i[0] == "load")
+
+
+def layout(rad, dtype: int, cfg: TbCfg) -> dict:
+    """Shared memory: the input TMA ring (tile + K*r halo) and, per
+    intermediate step, a ring of rz+1 planes in the step-1 frame (W1 x H1)."""
+    rz, ry, rx = rad
+    elem = ELEM[dtype]
+    q = 16 // elem
+    K = cfg.k
+    w0 = _round(cfg.bx + 2 * K * rx + q - 1, q)
+    h0 = cfg.by + 2 * K * ry
+    s0 = rz + 1 + cfg.prefetch
+    pl0 = _round(w0 * h0 * elem, 1024)
+    w1, h1 = cfg.bx + 2 * (K - 1) * rx, cfg.by + 2 * (K - 1) * ry
+    pl1 = _round(w1 * h1 * elem, 128)
+    off = s0 * pl0
+    rings = []
+    for _j in range(1, K):
+        rings.append({"off": off, "n": rz + 1})
+        off += (rz + 1) * pl1
+    data = _round(off, 8)
+    smem = data + 8 * 2 * s0 + 1024
+    hg = h1 // cfg.rpt if h1 % cfg.rpt == 0 else 0
+    nt = _round(w1 * hg, 32)
+    return {"rad": (rz, ry, rx), "w0": w0, "h0": h0, "s0": s0, "pl0": pl0, "w1": w1, "h1": h1,
+            "pl1": pl1, "hg": hg, "nt": nt, "rings": rings, "data": data, "smem": smem,
+            "cfg": cfg, "elem": elem, "q": q}
+
+
+def eligible(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> bool:
+    """Single input slot, z-star loads, 1 <= rz, radius <= MAX_RADIUS, fits."""
+    cfg = cfg or DEFAULT
+    if cfg.k < 2 or cfg.k % 2 or st.arity != 1 or dtype not in ELEM or not z_star(st):
+        return False
+    rad = slot_radius(st).get(0)
+    if rad is None or max(rad) > MAX_RADIUS or rad[0] < 1:
+        return False
+    lay = layout(rad, dtype, cfg)
+    if lay["w0"] > 256 or lay["h0"] > 256 or lay["hg"] == 0 or lay["nt"] + 32 > 1024:
+        return False
+    return lay["smem"] <= SMEM_BUDGET
+
+
+def blocks_per_sm(smem: int, nt: int) -> int:
+    return max(1, min(SMEM_PER_SM // (smem + 1024), 2048 // (nt + 32)))
+
+
+def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
+    """-> (source, kernel name, block, smem, geometry).
+
+    Each compute thread owns RPT points of the step-1 region (W1 x H1, rows
+    interleaved by H1/RPT so warps run along x) for every plane: its own
+    column of every step lives in registers (the pure-z operands), the centre
+    plane of each step is published in shared memory for the neighbours'
+    (dy, dx) operands. Per input plane: one mbarrier wait (TMA), one named
+    barrier, then step 1 .. K each one plane further behind."""
+    cfg = cfg or DEFAULT
+    rad = slot_radius(st)[0]
+    lay = layout(rad, dtype, cfg)
+    rz, ry, rx = rad
+    K, BX, BY, RPT = cfg.k, cfg.bx, cfg.by, cfg.rpt
+    NT, HG, W1, H1 = lay["nt"], lay["hg"], lay["w1"], lay["h1"]
+    NW = NT // 32
+    T = CTYPE[dtype]
+    q = lay["q"]
+    s0, pl0, w0, h0 = lay["s0"], lay["pl0"], lay["w0"], lay["h0"]
+    E = lay["elem"]
+    L = []
+    a = L.append
+    a(f'// generated by paper_2512_19851_b200/temporal.py — skeleton "tb" (K={K} fused sweeps) {cfg}')
+    a(f"typedef {T} T;")
+    a("struct __align__(64) Tmap { unsigned long long w[16]; };")
+    a("struct __align__(64) Params { Tmap tm;")
+    a("  unsigned long long src, bhome, adst;  // padded-box origins: A now, B (in place), A next")
+    a("  long long py, pz;")
+    a("  int npz, npy, npx, xoff, sz0, sz1, sy0, sy1, sx0, sx1, nbx, nby, zc, nzc; };")
+    L.append(_PTX_HELPERS)
+    a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
+    a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
+    a(f"__device__ __forceinline__ void plane_barrier() {{ asm volatile(\"bar.sync 1, {NT};\" ::: \"memory\"); }}")
+    minb = max(1, min(blocks_per_sm(lay["smem"], NT), 65536 // ((NT + 32) * 48)))
+    lay["min_blocks"] = minb
+    a(f'extern "C" __global__ void __launch_bounds__({NT + 32}, {minb})')
+    a("est_tb(const __grid_constant__ Params p) {")
+    a("  extern __shared__ __align__(1024) unsigned char smem[];")
+    a(f"  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + {lay['data']});")
+    a(f"  unsigned long long* empty = full + {s0};")
+    a("  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;")
+    a("  const int n_items = p.nbx * p.nby * p.nzc;")
+    a("  if (tid == 0) {")
+    a(f"    for (int i = 0; i < {s0}; ++i) {{ mbar_init(full + i, 1); mbar_init(empty + i, {NW}); }}")
+    a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
+    a("  }")
+    a("  __syncthreads();")
+
+    def item_decode(ind):
+        a(f"{ind}const int bx = item % p.nbx, rest = item / p.nbx;")
+        a(f"{ind}const int by = rest % p.nby, bzc = rest / p.nby;")
+        a(f"{ind}const int x0 = p.sx0 + bx * {BX}, y0 = p.sy0 + by * {BY};")
+        a(f"{ind}const int zs = p.sz0 + bzc * p.zc;")
+        a(f"{ind}const int nzl = min(p.zc, p.sz1 - zs);")
+        a(f"{ind}const int n0 = nzl + {2 * K * rz};")
+
+    # ---------------- producer warp
+    a(f"  if (warp == {NW}) {{")
+    a("    if (lane != 0) return;")
+    a("    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm) : \"memory\");")
+    a("    int fill = 0;")
+    a("    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+    item_decode("      ")
+    a(f"      const int xs = p.xoff + x0 - {K * rx};")
+    a(f"      const int xa = xs - (xs & {q - 1});")
+    a("      for (int k = 0; k < n0; ++k) {")
+    a(f"        const int g = fill + k, stg = g % {s0};")
+    a(f"        if (g >= {s0}) mbar_wait(empty + stg, ((g / {s0}) - 1) & 1);")
+    a(f"        mbar_expect(full + stg, {w0 * h0 * E});")
+    a(f"        tma_load3(smem + stg * {pl0}, &p.tm, xa, y0 - {K * ry}, zs - {K * rz} + k, full + stg);")
+    a("      }")
+    a("      fill += n0;")
+    a("    }")
+    a("    return;")
+    a("  }")
+    # ---------------- compute threads
+    a("  const T* __restrict__ asrc = reinterpret_cast<const T*>(p.src);")
+    a("  T* __restrict__ bmem = reinterpret_cast<T*>(p.bhome);")
+    a("  T* __restrict__ adst = reinterpret_cast<T*>(p.adst);")
+    a(f"  const bool act = tid < {W1 * HG};")
+    a(f"  const int lx = tid % {W1}, lyg = tid / {W1};")
+    # per-row thread constants (item independent)
+    for r in range(RPT):
+        ly = f"(lyg + {r * HG})"
+        a(f"  const int ly{r} = {ly};")
+        for j in range(2, K + 1):
+            lo_y, hi_y = (j - 1) * ry, H1 - (j - 1) * ry
+            lo_x, hi_x = (j - 1) * rx, W1 - (j - 1) * rx
+            a(f"  const bool inT{j}_{r} = act && ly{r} >= {lo_y} && ly{r} < {hi_y} && lx >= {lo_x} && lx < {hi_x};")
+        a(f"  const int so{r} = ly{r} * {W1} + lx;  // step-1 frame smem index")
+        a(f"  const int io{r} = (ly{r} + {ry}) * {w0} + lx + {rx};  // input frame (before the alignment shift)")
+    a("  int fill = 0;")
+    # register columns: c{j}_{r}_{k} = step-j value (j = 0: input) at the thread point, k = 0..2rz
+    for j in range(0, K):
+        for r in range(RPT):
+            a(f"  T {', '.join(f'c{j}_{r}_{k} = 0' for k in range(2 * rz + 1))};")
+    a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+    item_decode("    ")
+    a(f"    const int sh = (p.xoff + x0 - {K * rx}) & {q - 1};")
+    for r in range(RPT):
+        a(f"    const int gy{r} = y0 - {(K - 1) * ry} + ly{r}, gx{r} = x0 - {(K - 1) * rx} + lx;")
+        a(f"    const bool sxy{r} = act && gy{r} >= p.sy0 && gy{r} < p.sy1 && gx{r} >= p.sx0 && gx{r} < p.sx1;")
+        a(f"    const bool pxy{r} = act && gy{r} >= 0 && gy{r} < p.npy && gx{r} >= 0 && gx{r} < p.npx;")
+        a(f"    const long long go{r} = (long long)gy{r} * p.py + gx{r};")
+    a("    for (int t = 0; t < n0; ++t) {")
+    # prefetch out-of-S values of intermediate steps (home buffers), before any wait
+    for j in range(1, K):
+        home = "bmem" if j % 2 == 1 else "asrc"
+        a(f"      const int z{j} = zs - {(K - j) * rz} + t - {2 * j * rz};")
+        a(f"      const bool zi{j} = z{j} >= p.sz0 && z{j} < p.sz1, zp{j} = z{j} >= 0 && z{j} < p.npz;")
+        for r in range(RPT):
+            inT = "act" if j == 1 else f"inT{j}_{r}"
+            a(f"      T h{j}_{r} = (T)0;")
+            a(f"      if (t >= {2 * j * rz} && {inT} && zp{j} && pxy{r} && !(zi{j} && sxy{r}))"
+              f" h{j}_{r} = {home}[(long long)z{j} * p.pz + go{r}];  // outside S: stored value")
+    a(f"      {{ const int g = fill + t; mbar_wait(full + g % {s0}, (g / {s0}) & 1); }}")
+    a("      plane_barrier();")
+    a(f"      const T* inC = reinterpret_cast<const T*>(smem) + ((fill + t) % {s0}) * {pl0 // E} + sh;")
+    for r in range(RPT):
+        a(f"      c0_{r}_{2 * rz} = act ? inC[io{r}] : (T)0;")
+    for j in range(1, K + 1):
+        emit_step_b(a, st, dtype, lay, j)
+        if j == 1:
+            a(f"      if (t >= {rz}) {{ __syncwarp(); if (lane == 0) mbar_arrive(empty + (fill + t - {rz}) % {s0}); }}")
+    # rotate the register columns (step j's column only moves once step j ran)
+    for j in range(0, K):
+        cond = "true" if j == 0 else f"t >= {2 * j * rz}"
+        a(f"      if ({cond}) {{")
+        for r in range(RPT):
+            for k in range(2 * rz):
+                a(f"        c{j}_{r}_{k} = c{j}_{r}_{k + 1};")
+        a("      }")
+    a("    }")
+    a(f"    for (int k = (n0 > {rz} ? n0 - {rz} : 0); k < n0; ++k) if (lane == 0) mbar_arrive(empty + (fill + k) % {s0});")
+    a("    fill += n0;")
+    a("  }")
+    a("}")
+    src = "\n".join(L) + "\n"
+    lay["blocks_per_sm"] = minb
+    return src, "est_tb", (NT + 32, 1, 1), lay["smem"], lay
+
+
+def emit_step_b(a, st: StmtSig, dtype: int, lay: dict, j: int) -> None:
+    """Step j at input iteration t: index u = t - 2*j*rz, centre plane of the
+    previous step at index u + rz (input ring for j = 1, ring j-1 otherwise)."""
+    cfg = lay["cfg"]
+    K, RPT = cfg.k, cfg.rpt
+    rz, ry, rx = lay["rad"]
+    W1 = lay["w1"]
+    E = lay["elem"]
+    final = j == K
+    ind = "        "
+    a(f"      if (t >= {2 * j * rz}) {{  // step {j}")
+    a(f"{ind}const int u = t - {2 * j * rz};")
+    a(f"{ind}const int zj = zs - {(K - j) * rz} + u;")
+    a(f"{ind}const bool zin = zj >= p.sz0 && zj < p.sz1;")
+    a(f"{ind}const long long zoff = (long long)zj * p.pz;")
+    if j == 1:
+        a(f"{ind}const T* P = reinterpret_cast<const T*>(smem) + ((fill + t - {rz}) % {lay['s0']}) * {lay['pl0'] // E} + sh;")
+    else:
+        rp = lay["rings"][j - 2]
+        a(f"{ind}const T* P = reinterpret_cast<const T*>(smem + {rp['off']}) + ((t - {(2 * j - 1) * rz}) % {rp['n']}) * {lay['pl1'] // E};")
+    if not final:
+        rg = lay["rings"][j - 1]
+        a(f"{ind}T* W = reinterpret_cast<T*>(smem + {rg['off']}) + (u % {rg['n']}) * {lay['pl1'] // E};")
+    for r in range(RPT):
+        inT = "act" if j == 1 else f"inT{j}_{r}"
+        base = f"io{r}" if j == 1 else f"so{r}"
+        pitch = lay["w0"] if j == 1 else W1
+
+        def load(slot, off3, r=r, base=base, pitch=pitch):
+            dz, dy, dx = off3
+            if dz != 0 or (dy == 0 and dx == 0):
+                return f"c{j - 1}_{r}_{rz + dz}"
+            return f"P[{base} + {dy * pitch + dx}]"
+
+        lines, res = _emit_expr(st, dtype, load)
+        a(f"{ind}if ({inT}) {{")
+        a(f"{ind}  T v;")
+        a(f"{ind}  if (zin && sxy{r}) {{")
+        for ln in lines:
+            a(f"{ind}    {ln}")
+        a(f"{ind}    v = {res};")
+        if final:
+            a(f"{ind}    adst[zoff + go{r}] = v;")
+        elif j == K - 1:
+            a(f"{ind}    if (inT{K}_{r}) bmem[zoff + go{r}] = v;")
+        a(f"{ind}  }} else {{")
+        a(f"{ind}    v = {'(T)0' if final else f'h{j}_{r}'};")
+        a(f"{ind}  }}")
+        if not final:
+            a(f"{ind}  W[so{r}] = v;")
+            a(f"{ind}  c{j}_{r}_{2 * rz} = v;")
+        a(f"{ind}}}")
+    a("      }")
+
+
+def item_geometry(s_lo, s_hi, sm_count: int, lay: dict) -> dict:
+    """Work-item tiling of the output box S (padded coordinates)."""
+    cfg = lay["cfg"]
+    nz, ny, nx = (b - a for a, b in zip(s_lo, s_hi))
+    nbx, nby = -(-nx // cfg.bx), -(-ny // cfg.by)
+    zc = min(cfg.zchunk, nz)
+    nzc = -(-nz // zc)
+    n_items = nbx * nby * nzc
+    cap = sm_count * lay.get("min_blocks", 1)
+    blocks = min(n_items, cap) if cfg.persistent else n_items
+    return {"nbx": nbx, "nby": nby, "zc": zc, "nzc": nzc, "blocks": blocks}
+
+
+def pack_params(tmap: bytes, src: int, bhome: int, adst: int, buf, s_lo, s_hi, geo: dict) -> bytes:
+    """Params block (layout mirrored in `source`). Pointers are padded-box
+    origins (buffer base + xoff elements)."""
+    assert len(tmap) == 128
+    npz, npy, npx = buf.nz, buf.pz // buf.py, buf.ext[2] + 2 * buf.depth[2]
+    out = bytearray(tmap)
+    out += struct.pack("<QQQqq", src, bhome, adst, buf.py, buf.pz)
+    out += struct.pack("<14i", npz, npy, npx, buf.xoff, s_lo[0], s_hi[0], s_lo[1], s_hi[1],
+                       s_lo[2], s_hi[2], geo["nbx"], geo["nby"], geo["zc"], geo["nzc"])
+    return bytes(out) + b"\0" * ((-len(out)) % 64)
+
+
+def complement_boxes(buf, src_base: int, dst_base: int, s_lo, s_hi) -> list:
+    """Copy descriptors covering the padded box minus S (<= 6 boxes), from the
+    buffer at `src_base` to an identically laid out one at `dst_base`."""
+    from ._lib import EstBox
+
+    npx = buf.ext[2] + 2 * buf.depth[2]
+    n = (buf.nz, buf.pz // buf.py, npx)
+    (z0, y0, x0), (z1, y1, x1) = s_lo, s_hi
+    boxes = [((0, 0, 0), (z0, n[1], n[2])), ((z1, 0, 0), (n[0], n[1], n[2])),
+             ((z0, 0, 0), (z1, y0, n[2])), ((z0, y1, 0), (z1, n[1], n[2])),
+             ((z0, y0, 0), (z1, y1, x0)), ((z0, y0, x1), (z1, y1, n[2]))]
+    out = []
+    for lo, hi in boxes:
+        ext = [b - a for a, b in zip(lo, hi)]
+        if min(ext) <= 0:
+            continue
+        off = (buf.xoff + lo[0] * buf.pz + lo[1] * buf.py + lo[2]) * buf.elem
+        out.append(EstBox(src_base + off, dst_base + off, buf.py, buf.pz, buf.py, buf.pz,
+                          ext[2], ext[1], ext[0]))
+    return out

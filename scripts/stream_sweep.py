@@ -74,7 +74,7 @@ def main():
             for _ in range(reps):
                 job.run(it.dag)
             job.sync()
-            ts = [a.elapsed_ms(b) for a, b in ex.kernel_events]
+            ts = [a.elapsed_ms(b) for a, b, _t in ex.kernel_events]
             ex.time_kernels = False
             ms = statistics.median(ts)
             print(json.dumps({"cfg": name, "kernel_ms": ms, "glups": lups / ms / 1e6,

@@ -95,7 +95,7 @@ class FakeDevice:
 
     def launch(self, k, grid, params, stream=0):
         self.launches += 1
-        self.log.append(("launch", grid[0]))
+        self.log.append(("launch", grid[0], getattr(k, "name", "")))
 
     def tmap_3d(self, base, elem, dims, strides, box, l2_promotion=3):
         return base.to_bytes(8, "little").ljust(128, b"\0")

@@ -1,0 +1,194 @@
+"""GPU parity of the temporal-blocking skeleton (temporal.py): K fused
+ping-pong sweeps must be bit-identical to the oracle (fp64; fp32 within the
+north star's 1e-5, in fact bit-identical because the plan order is kept).
+
+Cases cover partial tiles, output slices that are not the full interior, a
+radius-2 and an asymmetric stencil, odd iteration counts (a leftover sweep on
+the node-by-node kernel), several batches with CUDA-graph replay, and that the
+fused kernel really ran (launch counts)."""
+
+import numpy as np
+import pytest
+
+from oracle.oracle import bits_equal, reference_execute_dag, strict_execute_dag
+from paper_2512_19851_b200.ir import add, cst, mul, ref, sub
+from paper_2512_19851_b200.programs import DagProgram, heat3d_program, heat3d_setup, heat3d_tree
+from paper_2512_19851_b200.session import GpuJob, run_program
+from paper_2512_19851_b200.wire import DTYPE_F32, encode_dag
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _chains_on(monkeypatch):
+    from paper_2512_19851_b200 import temporal
+    monkeypatch.setattr(temporal, "ENABLED", True)
+
+
+def _tb_launches(stats) -> int:
+    return sum(s.gpu_launches for b in stats for s in b)
+
+
+@pytest.mark.parametrize("n,iters", [(24, 4), (40, 8), (67, 6), (64, 13), (130, 4)])
+def test_heat3d_chains_bit_exact(n, iters):
+    prog = DagProgram()
+    heat3d_program(prog, n, iters, seed_fills=12)
+    want = strict_execute_dag(prog.dag, prog.shapes)
+    job, stats = run_program(prog, fused=True)
+    try:
+        assert job.executors[0]._scratch, "temporal chain did not run"
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), (n, iters, aid)
+    finally:
+        job.close()
+
+
+def _star(u, box, radius=1, axes=(0, 1, 2)):
+    """Ordered sum of the +/- radius neighbours along `axes`, times a constant."""
+    def sh(axis, d):
+        return ref(u, tuple(slice(lo + (d if k == axis else 0), hi + (d if k == axis else 0))
+                            for k, (lo, hi) in enumerate(box)))
+    s = None
+    for ax in axes:
+        for d in range(1, radius + 1):
+            for dd in (-d, d):
+                term = sh(ax, dd)
+                s = term if s is None else add(s, term)
+    return mul(cst(0.0625), sub(s, ref(u, tuple(slice(lo, hi) for lo, hi in box))))
+
+
+@pytest.mark.parametrize("box,radius", [
+    (((2, 37), (1, 38), (3, 36)), 1),     # S off-centre, partial tiles in x and y
+    (((2, 38), (2, 38), (2, 38)), 2),     # radius-2 star (depth 2)
+    (((3, 30), (5, 33), (2, 38)), 2),
+])
+def test_subbox_chains_bit_exact(box, radius):
+    n = 40
+    prog = DagProgram()
+    u1, u2 = heat3d_setup(prog, n, seed_fills=10)
+    for _ in range(8):
+        prog.assign(u2, box, _star(u1, box, radius))
+        u1, u2 = u2, u1
+    want = reference_execute_dag(prog.dag, prog.shapes)
+    job, _ = run_program(prog)
+    try:
+        assert job.executors[0]._scratch
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), (box, radius, aid)
+    finally:
+        job.close()
+
+
+def test_asymmetric_offsets_bit_exact():
+    """Asymmetric z-star stencil (dz in {-2, 1}, in-plane (1,-1) and (-1,0))."""
+    n = 36
+    prog = DagProgram()
+    u1, u2 = heat3d_setup(prog, n, seed_fills=8)
+    box = ((2, 34), (1, 35), (2, 35))
+
+    def at(u, dz, dy, dx):
+        return ref(u, tuple(slice(lo + d, hi + d) for (lo, hi), d in zip(box, (dz, dy, dx))))
+    for _ in range(6):
+        e = add(mul(cst(0.5), at(u1, -2, 0, 0)), mul(cst(0.25), at(u1, 0, 1, -1)))
+        e = sub(e, mul(cst(0.125), at(u1, 1, 0, 0)))
+        e = add(e, at(u1, 0, -1, 0))
+        prog.assign(u2, box, e)
+        u1, u2 = u2, u1
+    want = reference_execute_dag(prog.dag, prog.shapes)
+    job, _ = run_program(prog)
+    try:
+        assert job.executors[0]._scratch
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), aid
+    finally:
+        job.close()
+
+
+def test_heat3d_fp32_chains():
+    prog = DagProgram()
+    heat3d_program(prog, 48, 8, seed_fills=10, dtype=DTYPE_F32)
+    want = reference_execute_dag(prog.dag, prog.shapes, prog.dtypes)
+    job, _ = run_program(prog)
+    try:
+        assert job.executors[0]._scratch
+        for aid in prog.shapes:
+            got = job.fetch(aid)
+            assert got.dtype == np.float32
+            np.testing.assert_allclose(got, want[aid], rtol=1e-5, atol=1e-5 * np.abs(want[aid]).max())
+            assert bits_equal(got, want[aid])
+    finally:
+        job.close()
+
+
+def test_repeated_batches_graph_replay_bit_exact():
+    """Steady-state batches replay a captured CUDA graph holding the chain kernels."""
+    n, per, batches = 48, 10, 5
+    setup = DagProgram()
+    u1, u2 = heat3d_setup(setup, n, seed_fills=10)
+    step = DagProgram()
+    for a in sorted(setup.shapes):
+        step.builder.declare_array(a, setup.shapes[a])
+    uu1, uu2 = u1, u2
+    for _ in range(per):
+        step.assign(uu2, (slice(1, -1),) * 3, heat3d_tree(uu1))
+        uu1, uu2 = uu2, uu1
+    full = DagProgram()
+    a1, a2 = heat3d_setup(full, n, seed_fills=10)
+    for _ in range(per * batches):
+        full.assign(a2, (slice(1, -1),) * 3, heat3d_tree(a1))
+        a1, a2 = a2, a1
+    want = strict_execute_dag(full.dag, full.shapes)
+    blob = encode_dag(step.dag)
+    with GpuJob() as job:
+        for aid in sorted(setup.shapes):
+            job.create_array(setup.shapes[aid])
+        job.run(setup.dag)
+        stats = [job.run_bytes(blob) for _ in range(batches)]
+        assert job.executors[0].replays >= 2
+        # 10 sweeps = 4 chains of 2 (chain count kept even) + 2 single sweeps
+        assert stats[1][0].gpu_launches == 4 + 2 + 1
+        for aid in setup.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), aid
+
+
+def test_chain_disabled_equals_enabled():
+    prog = DagProgram()
+    heat3d_program(prog, 56, 8, seed_fills=12)
+    outs = []
+    for on in (True, False):
+        job = GpuJob()
+        job_stats = None
+        try:
+            for aid in sorted(prog.shapes):
+                job.create_array(prog.shapes[aid])
+            job.executors[0].temporal = on
+            job_stats = job.run(prog.dag)
+            outs.append([job.fetch(a) for a in sorted(prog.shapes)])
+            assert bool(job.executors[0]._scratch) == on
+        finally:
+            job.close()
+        assert job_stats[0].kernel_launches == len(prog.dag.nodes)
+    for x, y in zip(*outs):
+        assert bits_equal(x, y)
+
+
+def test_non_z_star_chain_runs_node_by_node():
+    """A diagonal (dz, dx) load is not chainable: no twin, still bit-exact."""
+    n = 32
+    prog = DagProgram()
+    u1, u2 = heat3d_setup(prog, n, seed_fills=6)
+    box = ((1, 31), (1, 31), (1, 31))
+
+    def at(u, dz, dy, dx):
+        return ref(u, tuple(slice(lo + d, hi + d) for (lo, hi), d in zip(box, (dz, dy, dx))))
+    for _ in range(4):
+        prog.assign(u2, box, add(at(u1, -1, 0, 1), mul(cst(0.5), at(u1, 1, 0, 0))))
+        u1, u2 = u2, u1
+    want = reference_execute_dag(prog.dag, prog.shapes)
+    job, _ = run_program(prog)
+    try:
+        assert not job.executors[0]._scratch
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), aid
+    finally:
+        job.close()

@@ -1,0 +1,151 @@
+"""Temporal chains (temporal.py) on the host side, CPU with the device test
+double: which nodes fuse, that per-node bookkeeping (epochs, rounds, launch
+counts) equals unfused execution, the twin buffer and its complement copy,
+and the generated kernel's shape."""
+
+import pytest
+
+from fakedev import FakeDevice
+from paper_2512_19851_b200 import codegen, temporal
+from paper_2512_19851_b200.analysis import compile_plan
+from paper_2512_19851_b200.exchange import GpuExchangeManager
+from paper_2512_19851_b200.executor import GpuExecutor
+from paper_2512_19851_b200.programs import DagProgram, heat3d_iterations, heat3d_setup, heat3d_tree
+from paper_2512_19851_b200.tiles import ArrayInfo, GpuTileStore, decompose
+from paper_2512_19851_b200.wire import DTYPE_F32, DTYPE_F64
+
+
+def _executor(shapes, workers=1, odf=1, temporal_on=True):
+    dev = FakeDevice()
+    shape = next(iter(shapes.values()))
+    decomp = decompose(shape, workers, odf)
+    owned = [c for c in decomp.all_coords() if decomp.owner_map(workers)[c] == 0]
+    store = GpuTileStore(dev, decomp, owned)
+    for a in sorted(shapes):
+        store.create_array(ArrayInfo(a, shapes[a]))
+    mgr = GpuExchangeManager(store, 0, decomp.owner_map(workers))
+    ex = GpuExecutor(store, mgr)
+    ex.temporal = temporal_on
+    return ex, store, mgr, dev
+
+
+def _heat(iters, n=16):
+    setup, step = DagProgram(), DagProgram()
+    u1, u2 = heat3d_setup(setup, n)
+    for a in sorted(setup.shapes):
+        step.builder.declare_array(a, setup.shapes[a])
+    heat3d_iterations(step, u1, u2, iters)
+    return setup, step
+
+
+def _names(dev):
+    return [e[2] for e in dev.log if e[0] == "launch"]
+
+
+@pytest.mark.parametrize("iters,fused", [(4, 4), (5, 4), (7, 4), (8, 8), (3, 0), (100, 100), (10, 8)])
+def test_chain_cut(iters, fused):
+    setup, step = _heat(iters)
+    ex, store, mgr, dev = _executor(setup.shapes)
+    ex.execute_batch(setup.dag)
+    plans = [compile_plan(n, step.dag.ast_table) for n in step.dag.nodes]
+    sched = ex.temporal_schedule(step.dag, plans)
+    K = ex.tb_cfg.k
+    leads = [nid for nid, v in sched.items() if v[0] == "lead"]
+    assert len(sched) == fused
+    assert len(leads) == fused // K
+    dev.log.clear()
+    stats = ex.execute_batch(step.dag)
+    names = _names(dev)
+    assert names.count("est_tb") == fused // K
+    assert names.count("est_stream") == iters - fused
+    assert stats.kernel_launches == iters  # reference definition: one per node per tile
+    assert stats.gpu_launches == len(names) + (1 if fused else 0)  # + complement copy
+
+
+def test_bookkeeping_matches_unfused():
+    for iters in (4, 6, 9):
+        setup, step = _heat(iters)
+        res = []
+        for on in (True, False):
+            ex, store, mgr, dev = _executor(setup.shapes, temporal_on=on)
+            ex.execute_batch(setup.dag)
+            st = [ex.execute_batch(step.dag, b"k") for _ in range(4)]
+            res.append(({a: (store.local_epoch(a), store.ghost_epoch(a)) for a in store.arrays},
+                        dict(mgr.rounds_started),
+                        [(s.nodes_executed, s.kernel_launches, s.rounds, s.net_messages) for s in st]))
+        assert res[0] == res[1], iters
+
+
+def test_twin_buffer_and_complement_copy():
+    setup, step = _heat(4, n=16)
+    ex, store, mgr, dev = _executor(setup.shapes)
+    ex.execute_batch(setup.dag)
+    dev.copies.clear()
+    ex.execute_batch(step.dag)
+    a = step.dag.nodes[0].statements[0].inputs[0]
+    twin = ex._scratch[a]
+    home = next(iter(store.tiles.values())).buffers[a]
+    assert (twin.py, twin.pz, twin.xoff, twin.nbytes) == (home.py, home.pz, home.xoff, home.nbytes)
+    strips = [c for c in dev.copies if c[0] == "strip"]
+    # padded box 18^3 minus S = [1,17)^3 in padded coords ([2,16) after depth 1) -> 6 boxes
+    assert len(strips) == 6
+    total = sum(c[3] * c[4] * c[5] for c in strips)
+    assert total == 18 ** 3 - 14 ** 3
+    assert all(c[2] - twin.ptr == c[1] - home.ptr for c in strips)
+    ex.release_scratch()
+    assert twin.ptr == 0
+
+
+def test_no_chains_with_several_tiles_or_workers():
+    setup, step = _heat(8, n=16)
+    for workers, odf in ((1, 2), (2, 1)):
+        ex, store, mgr, dev = _executor(setup.shapes, workers, odf)
+        plans = [compile_plan(n, step.dag.ast_table) for n in step.dag.nodes]
+        assert ex.temporal_schedule(step.dag, plans) == {}
+
+
+def test_chain_requires_same_statement_and_ping_pong():
+    prog = DagProgram()
+    u1, u2 = heat3d_setup(prog, 16)
+    u3 = prog.create_array((16, 16, 16))
+    interior = (slice(1, -1),) * 3
+    prog.assign(u2, interior, heat3d_tree(u1))
+    prog.assign(u1, interior, heat3d_tree(u2))
+    prog.assign(u3, interior, heat3d_tree(u1))   # breaks the ping-pong
+    prog.assign(u1, interior, heat3d_tree(u3))
+    ex, store, mgr, dev = _executor(prog.shapes)
+    plans = [compile_plan(n, prog.dag.ast_table) for n in prog.dag.nodes]
+    sched = ex.temporal_schedule(prog.dag, plans)
+    assert sched == {}
+
+
+def test_generated_kernel_shape():
+    prog = DagProgram()
+    heat3d_setup(prog, 32)
+    a, b = 0, 1
+    prog.assign(b, (slice(1, -1),) * 3, heat3d_tree(a))
+    plan = compile_plan(prog.dag.nodes[-1], prog.dag.ast_table)
+    sig = codegen.stmt_sig(plan.statements[0], 3)
+    for dt in (DTYPE_F64, DTYPE_F32):
+        assert temporal.eligible(sig, dt)
+        src, name, block, smem, lay = temporal.source(sig, dt)
+        assert name == "est_tb" and block[0] == lay["nt"] + 32 and lay["min_blocks"] >= 1
+        assert smem <= temporal.SMEM_BUDGET
+        assert "cp.async.bulk.tensor.3d" in src and "bar.sync 1" in src
+        assert "__dadd_rn" in src if dt == DTYPE_F64 else "__fadd_rn" in src
+
+
+def test_z_star_required():
+    """Loads off the centre plane must be pure z offsets (register columns)."""
+    prog = DagProgram()
+    a, b = heat3d_setup(prog, 16)
+    box = (slice(1, -1),) * 3
+    from paper_2512_19851_b200.ir import add
+    from paper_2512_19851_b200.ir import ref as r_
+    diag = add(r_(a, (slice(0, -2), slice(1, -1), slice(2, None))), r_(a, (slice(2, None), slice(1, -1), slice(1, -1))))
+    prog.assign(b, box, diag)
+    plan = compile_plan(prog.dag.nodes[-1], prog.dag.ast_table)
+    assert not temporal.eligible(codegen.stmt_sig(plan.statements[0], 3), DTYPE_F64)
+    prog.assign(b, box, heat3d_tree(a))
+    plan = compile_plan(prog.dag.nodes[-1], prog.dag.ast_table)
+    assert temporal.eligible(codegen.stmt_sig(plan.statements[0], 3), DTYPE_F64)
