@@ -54,6 +54,7 @@ class TbCfg:
     zchunk: int = 128       # planes per item
     l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
     persistent: bool = False
+    minb: int = 0           # __launch_bounds__ min blocks per SM (0: from smem/threads, >= 48 regs)
 
 
 def _env_cfg() -> TbCfg:
@@ -62,7 +63,7 @@ def _env_cfg() -> TbCfg:
     return TbCfg(k=int(e("EST_TB_K", d.k)), bx=int(e("EST_TB_BX", d.bx)), by=int(e("EST_TB_BY", d.by)),
                  rpt=int(e("EST_TB_RPT", d.rpt)), prefetch=int(e("EST_TB_PREFETCH", d.prefetch)),
                  zchunk=int(e("EST_TB_ZCHUNK", d.zchunk)), l2promo=int(e("EST_TB_L2PROMO", d.l2promo)),
-                 persistent=e("EST_TB_PERSISTENT", "0") == "1")
+                 persistent=e("EST_TB_PERSISTENT", "0") == "1", minb=int(e("EST_TB_MINB", d.minb)))
 
 
 DEFAULT = _env_cfg()
@@ -80,7 +81,8 @@ def z_star(st: StmtSig) -> bool:
 
 def layout(rad, dtype: int, cfg: TbCfg) -> dict:
     """Shared memory: the input TMA ring (tile + K*r halo) and, per
-    intermediate step, a ring of rz+1 planes in the step-1 frame (W1 x H1)."""
+    intermediate step, a ring of 2rz+2 planes in the step-1 frame (W1 x H1)
+    with one mbarrier per plane slot (count = compute warps)."""
     rz, ry, rx = rad
     elem = ELEM[dtype]
     q = 16 // elem
@@ -93,11 +95,12 @@ def layout(rad, dtype: int, cfg: TbCfg) -> dict:
     pl1 = _round(w1 * h1 * elem, 128)
     off = s0 * pl0
     rings = []
+    nr = 2 * rz + 2  # slots: a warp may run one plane ahead (split arrive / wait)
     for _j in range(1, K):
-        rings.append({"off": off, "n": rz + 1})
-        off += (rz + 1) * pl1
+        rings.append({"off": off, "n": nr})
+        off += nr * pl1
     data = _round(off, 8)
-    smem = data + 8 * 2 * s0 + 1024
+    smem = data + 8 * (2 * s0 + (K - 1) * nr) + 1024
     hg = h1 // cfg.rpt if h1 % cfg.rpt == 0 else 0
     nt = _round(w1 * hg, 32)
     return {"rad": (rz, ry, rx), "w0": w0, "h0": h0, "s0": s0, "pl0": pl0, "w1": w1, "h1": h1,
@@ -155,8 +158,7 @@ def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
     L.append(_PTX_HELPERS)
     a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
     a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
-    a(f"__device__ __forceinline__ void plane_barrier() {{ asm volatile(\"bar.sync 1, {NT};\" ::: \"memory\"); }}")
-    minb = max(1, min(blocks_per_sm(lay["smem"], NT), 65536 // ((NT + 32) * 48)))
+    minb = cfg.minb or max(1, min(blocks_per_sm(lay["smem"], NT), 65536 // ((NT + 32) * 96)))
     lay["min_blocks"] = minb
     a(f'extern "C" __global__ void __launch_bounds__({NT + 32}, {minb})')
     a("est_tb(const __grid_constant__ Params p) {")
@@ -167,6 +169,7 @@ def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
     a("  const int n_items = p.nbx * p.nby * p.nzc;")
     a("  if (tid == 0) {")
     a(f"    for (int i = 0; i < {s0}; ++i) {{ mbar_init(full + i, 1); mbar_init(empty + i, {NW}); }}")
+    a(f"    for (int i = 0; i < {(K - 1) * lay['rings'][0]['n'] if K > 1 else 0}; ++i) mbar_init(empty + {s0} + i, {NW});")
     a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
     a("  }")
     a("  __syncthreads();")
@@ -206,7 +209,7 @@ def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
     a(f"  const int lx = tid % {W1}, lyg = tid / {W1};")
     # per-row thread constants (item independent)
     for r in range(RPT):
-        ly = f"(lyg + {r * HG})"
+        ly = f"(lyg * {RPT} + {r})"
         a(f"  const int ly{r} = {ly};")
         for j in range(2, K + 1):
             lo_y, hi_y = (j - 1) * ry, H1 - (j - 1) * ry
@@ -215,6 +218,9 @@ def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
         a(f"  const int so{r} = ly{r} * {W1} + lx;  // step-1 frame smem index")
         a(f"  const int io{r} = (ly{r} + {ry}) * {w0} + lx + {rx};  // input frame (before the alignment shift)")
     a("  int fill = 0;")
+    for j in range(1, K):
+        a(f"  unsigned long long* rb{j} = empty + {s0 + (j - 1) * lay['rings'][0]['n']};  // ring {j} slot barriers")
+        a(f"  int f{j} = 0;  // step-{j} planes produced so far (all items)")
     # register columns: c{j}_{r}_{k} = step-j value (j = 0: input) at the thread point, k = 0..2rz
     for j in range(0, K):
         for r in range(RPT):
@@ -227,6 +233,11 @@ def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
         a(f"    const bool sxy{r} = act && gy{r} >= p.sy0 && gy{r} < p.sy1 && gx{r} >= p.sx0 && gx{r} < p.sx1;")
         a(f"    const bool pxy{r} = act && gy{r} >= 0 && gy{r} < p.npy && gx{r} >= 0 && gx{r} < p.npx;")
         a(f"    const long long go{r} = (long long)gy{r} * p.py + gx{r};")
+    a(f"    const bool fast = (x0 - {(K - 1) * rx} >= p.sx0) && (x0 + {BX + (K - 1) * rx} <= p.sx1) &&"
+      f" (y0 - {(K - 1) * ry} >= p.sy0) && (y0 + {BY + (K - 1) * ry} <= p.sy1);")
+    a("    if (fast) {")
+    emit_fast_loop(a, st, dtype, lay)
+    a("    } else {")
     a("    for (int t = 0; t < n0; ++t) {")
     # prefetch out-of-S values of intermediate steps (home buffers), before any wait
     for j in range(1, K):
@@ -239,7 +250,6 @@ def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
             a(f"      if (t >= {2 * j * rz} && {inT} && zp{j} && pxy{r} && !(zi{j} && sxy{r}))"
               f" h{j}_{r} = {home}[(long long)z{j} * p.pz + go{r}];  // outside S: stored value")
     a(f"      {{ const int g = fill + t; mbar_wait(full + g % {s0}, (g / {s0}) & 1); }}")
-    a("      plane_barrier();")
     a(f"      const T* inC = reinterpret_cast<const T*>(smem) + ((fill + t) % {s0}) * {pl0 // E} + sh;")
     for r in range(RPT):
         a(f"      c0_{r}_{2 * rz} = act ? inC[io{r}] : (T)0;")
@@ -256,13 +266,114 @@ def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
                 a(f"        c{j}_{r}_{k} = c{j}_{r}_{k + 1};")
         a("      }")
     a("    }")
+    a("    }  // general path")
     a(f"    for (int k = (n0 > {rz} ? n0 - {rz} : 0); k < n0; ++k) if (lane == 0) mbar_arrive(empty + (fill + k) % {s0});")
     a("    fill += n0;")
+    for j in range(1, K):
+        a(f"    f{j} += nzl + {2 * (K - j) * rz};")
     a("  }")
     a("}")
     src = "\n".join(L) + "\n"
     lay["blocks_per_sm"] = minb
     return src, "est_tb", (NT + 32, 1, 1), lay["smem"], lay
+
+
+def emit_fast_loop(a, st: StmtSig, dtype: int, lay: dict) -> None:
+    """Items whose whole step-1 region lies inside S in y/x: no per-point
+    S tests (planes outside S's z range take a uniform branch), store
+    pointers advanced per plane, ring slots as counters, and the plane loop
+    unrolled 2rz+1 times so the register columns rotate by renaming."""
+    cfg = lay["cfg"]
+    K, RPT = cfg.k, cfg.rpt
+    rz, ry, rx = lay["rad"]
+    s0, E = lay["s0"], lay["elem"]
+    pl0, pl1 = lay["pl0"] // E, lay["pl1"] // E
+    Z = 2 * rz + 1          # register column length = unroll factor
+    ind = "      "
+    a(f"{ind}const long long pz = p.pz;")
+    for r in range(RPT):
+        a(f"{ind}T* bp{r} = bmem + (long long)(zs - {rz}) * pz + go{r};  // step K-1 (B) plane 0")
+        a(f"{ind}T* ap{r} = adst + (long long)zs * pz + go{r};  // step K (A next) plane 0")
+    a(f"{ind}int is = fill % {s0}, ip = (fill / {s0}) & 1;  // input slot / phase of index t")
+    a(f"{ind}const T* ring0 = reinterpret_cast<const T*>(smem) + sh;")
+    a(f"{ind}for (int t0 = 0; t0 < n0; t0 += {Z}) {{")
+    for m in range(Z):
+        # logical column index k (0 = oldest of the window) lives in name (k + m) % Z
+        def col(j, r, k, m=m):
+            return f"c{j}_{r}_{(k + m) % Z}"
+        a(f"{ind}  if (t0 + {m} < n0) {{  // plane iteration t = t0 + {m}")
+        a(f"{ind}  const int t = t0 + {m};")
+        a(f"{ind}  mbar_wait(full + is, ip);")
+        a(f"{ind}  {{ const T* inC = ring0 + is * {pl0};")
+        for r in range(RPT):
+            a(f"{ind}    {col(0, r, 2 * rz)} = inC[io{r}];")
+        a(f"{ind}  }}")
+        a(f"{ind}  int ir = is - {rz}; if (ir < 0) ir += {s0};  // slot of index t - rz")
+        for j in range(1, K + 1):
+            final = j == K
+            a(f"{ind}  if (t >= {2 * j * rz}) {{  // step {j}")
+            a(f"{ind}    const bool zin = (zs - {(K - j) * rz} + t - {2 * j * rz}) >= p.sz0 &&"
+              f" (zs - {(K - j) * rz} + t - {2 * j * rz}) < p.sz1;")
+            if j == 1:
+                a(f"{ind}    const T* P = ring0 + ir * {pl0};")
+            else:
+                rp = lay["rings"][j - 2]
+                nr = rp["n"]
+                a(f"{ind}    const int gr = f{j - 1} + t - {(2 * j - 1) * rz};")
+                a(f"{ind}    mbar_wait(rb{j - 1} + gr % {nr}, (gr / {nr}) & 1);")
+                a(f"{ind}    const T* P = reinterpret_cast<const T*>(smem + {rp['off']}) + (gr % {nr}) * {pl1};")
+            if not final:
+                rg = lay["rings"][j - 1]
+                a(f"{ind}    const int gw = f{j} + t - {2 * j * rz};")
+                a(f"{ind}    T* Wr = reinterpret_cast<T*>(smem + {rg['off']}) + (gw % {rg['n']}) * {pl1};")
+                home = "bmem" if j % 2 == 1 else "asrc"
+                a(f"{ind}    const long long zo = (long long)(zs - {(K - j) * rz} + t - {2 * j * rz}) * pz;")
+            a(f"{ind}    if (zin) {{")
+            for r in range(RPT):
+                inT = "act" if j == 1 else f"inT{j}_{r}"
+                base = f"io{r}" if j == 1 else f"so{r}"
+                pitch = lay["w0"] if j == 1 else lay["w1"]
+
+                def load(slot, off3, r=r, base=base, pitch=pitch, j=j):
+                    dz, dy, dx = off3
+                    if dz != 0 or (dy == 0 and dx == 0):
+                        return col(j - 1, r, rz + dz)
+                    if dx == 0 and 0 <= r + dy < RPT:
+                        return col(j - 1, r + dy, rz)
+                    return f"P[{base} + {dy * pitch + dx}]"
+
+                lines, res = _emit_expr(st, dtype, load)
+                a(f"{ind}      if ({inT}) {{")
+                for ln in lines:
+                    a(f"{ind}        {ln}")
+                if final:
+                    a(f"{ind}        *ap{r} = {res};")
+                else:
+                    a(f"{ind}        Wr[so{r}] = {res};")
+                    a(f"{ind}        {col(j, r, 2 * rz)} = {res};")
+                    if j == K - 1:
+                        a(f"{ind}        if (inT{K}_{r}) *bp{r} = {res};")
+                a(f"{ind}      }}")
+            a(f"{ind}    }}")
+            if not final:
+                a(f"{ind}    else {{  // plane outside S: the array's stored value")
+                for r in range(RPT):
+                    inT = "act" if j == 1 else f"inT{j}_{r}"
+                    a(f"{ind}      if ({inT}) {{ const T v = {home}[zo + go{r}]; Wr[so{r}] = v; {col(j, r, 2 * rz)} = v; }}")
+                a(f"{ind}    }}")
+            for r in range(RPT):
+                if final:
+                    a(f"{ind}    ap{r} += pz;")
+                elif j == K - 1:
+                    a(f"{ind}    bp{r} += pz;")
+            if not final:
+                a(f"{ind}    __syncwarp(); if (lane == 0) mbar_arrive(rb{j} + gw % {lay['rings'][j - 1]['n']});")
+            a(f"{ind}  }}")
+            if j == 1:
+                a(f"{ind}  if (t >= {rz}) {{ __syncwarp(); if (lane == 0) mbar_arrive(empty + ir); }}")
+        a(f"{ind}  if (++is == {s0}) {{ is = 0; ip ^= 1; }}")
+        a(f"{ind}  }}")
+    a(f"{ind}}}")
 
 
 def emit_step_b(a, st: StmtSig, dtype: int, lay: dict, j: int) -> None:
@@ -284,10 +395,14 @@ def emit_step_b(a, st: StmtSig, dtype: int, lay: dict, j: int) -> None:
         a(f"{ind}const T* P = reinterpret_cast<const T*>(smem) + ((fill + t - {rz}) % {lay['s0']}) * {lay['pl0'] // E} + sh;")
     else:
         rp = lay["rings"][j - 2]
-        a(f"{ind}const T* P = reinterpret_cast<const T*>(smem + {rp['off']}) + ((t - {(2 * j - 1) * rz}) % {rp['n']}) * {lay['pl1'] // E};")
+        nr = rp["n"]
+        a(f"{ind}const int gr = f{j - 1} + t - {(2 * j - 1) * rz};  // step-{j - 1} plane read")
+        a(f"{ind}mbar_wait(rb{j - 1} + gr % {nr}, (gr / {nr}) & 1);")
+        a(f"{ind}const T* P = reinterpret_cast<const T*>(smem + {rp['off']}) + (gr % {nr}) * {lay['pl1'] // E};")
     if not final:
         rg = lay["rings"][j - 1]
-        a(f"{ind}T* W = reinterpret_cast<T*>(smem + {rg['off']}) + (u % {rg['n']}) * {lay['pl1'] // E};")
+        a(f"{ind}const int gw = f{j} + u;")
+        a(f"{ind}T* W = reinterpret_cast<T*>(smem + {rg['off']}) + (gw % {rg['n']}) * {lay['pl1'] // E};")
     for r in range(RPT):
         inT = "act" if j == 1 else f"inT{j}_{r}"
         base = f"io{r}" if j == 1 else f"so{r}"
@@ -297,6 +412,8 @@ def emit_step_b(a, st: StmtSig, dtype: int, lay: dict, j: int) -> None:
             dz, dy, dx = off3
             if dz != 0 or (dy == 0 and dx == 0):
                 return f"c{j - 1}_{r}_{rz + dz}"
+            if dx == 0 and 0 <= r + dy < RPT:
+                return f"c{j - 1}_{r + dy}_{rz}"  # the thread's own neighbouring row
             return f"P[{base} + {dy * pitch + dx}]"
 
         lines, res = _emit_expr(st, dtype, load)
@@ -317,6 +434,8 @@ def emit_step_b(a, st: StmtSig, dtype: int, lay: dict, j: int) -> None:
             a(f"{ind}  W[so{r}] = v;")
             a(f"{ind}  c{j}_{r}_{2 * rz} = v;")
         a(f"{ind}}}")
+    if not final:
+        a(f"{ind}__syncwarp(); if (lane == 0) mbar_arrive(rb{j} + gw % {lay['rings'][j - 1]['n']});")
     a("      }")
 
 

@@ -131,7 +131,7 @@ def test_generated_kernel_shape():
         src, name, block, smem, lay = temporal.source(sig, dt)
         assert name == "est_tb" and block[0] == lay["nt"] + 32 and lay["min_blocks"] >= 1
         assert smem <= temporal.SMEM_BUDGET
-        assert "cp.async.bulk.tensor.3d" in src and "bar.sync 1" in src
+        assert "cp.async.bulk.tensor.3d" in src and "mbarrier.arrive" in src
         assert "__dadd_rn" in src if dt == DTYPE_F64 else "__fadd_rn" in src
 
 
