@@ -75,6 +75,8 @@ def standard_sources() -> list:
                 plan = compile_plan(node, dag.ast_table)
                 for skel in ("auto", "point"):
                     srcs.add(kernel_source_for(plan, rank, dt, skel)[0])
+                if rank == 2:
+                    srcs.add(kernel_source_for(plan, rank, dt, "auto", small=True)[0])
                 if rank == 3 and len(plan.statements) == 1:
                     from . import temporal
                     from .codegen import stmt_sig

@@ -227,16 +227,16 @@ est_node(const __grid_constant__ Params p) {{
 # --------------------------------------------------------------------------
 # "stream" skeleton (2.5-D, TMA): see stream.py
 
-def stream_eligible(stmts, rank: int, dtype: int = DTYPE_F64) -> bool:
+def stream_eligible(stmts, rank: int, dtype: int = DTYPE_F64, cfg=None) -> bool:
     from . import stream
 
-    return stream.eligible(stmts, rank, dtype)
+    return stream.eligible(stmts, rank, dtype, cfg)
 
 
-def stream_source(sig: NodeSig, rank: int) -> tuple:
+def stream_source(sig: NodeSig, rank: int, cfg=None) -> tuple:
     from . import stream
 
-    return stream.source(sig, rank)
+    return stream.source(sig, rank, cfg)
 
 
 # --------------------------------------------------------------------------
@@ -245,23 +245,25 @@ def stream_source(sig: NodeSig, rank: int) -> tuple:
 _SRC_CACHE: dict = {}
 
 
-def kernel_source_for(plan, rank: int, dtype: int, skeleton: str = "auto") -> tuple:
+def kernel_source_for(plan, rank: int, dtype: int, skeleton: str = "auto", small: bool = False) -> tuple:
     """-> (source, kernel name, block, smem, items per launch, geometry, NodeSig).
 
-    Memoised on the plan instructions, so repeated nodes cost a dict lookup.
+    `small`: the node's boxes are small (stream.SMALL_2D_POINTS) - rank-2
+    stream nodes then use shorter tiles. Memoised on the plan instructions,
+    so repeated nodes cost a dict lookup.
     """
     from . import stream
 
-    key = (tuple(p.instructions for p in plan.statements), rank, dtype, skeleton, stream.cfg_for(rank))
+    cfg = stream.cfg_for(rank, small)
+    key = (tuple(p.instructions for p in plan.statements), rank, dtype, skeleton, cfg)
     hit = _SRC_CACHE.get(key)
     if hit is not None:
         return hit
     stmts = tuple(stmt_sig(p, rank) for p in plan.statements)
     skel = "point"
-    if skeleton in ("auto", "stream") and stream_eligible(stmts, rank, dtype):
+    if skeleton in ("auto", "stream") and stream_eligible(stmts, rank, dtype, cfg):
         skel = "stream"
     sig = NodeSig(dtype, stmts, skel)
-    gen = stream_source if skel == "stream" else point_source
-    res = (*gen(sig, rank), sig)
+    res = (*(stream_source(sig, rank, cfg) if skel == "stream" else point_source(sig, rank)), sig)
     _SRC_CACHE[key] = res
     return res

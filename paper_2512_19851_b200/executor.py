@@ -529,8 +529,9 @@ class GpuExecutor:
             return
         info = self.store.arrays[plan.statements[0].output]
         rank, dtype = info.rank, info.dtype
+        small = rank == 2 and sum(n[0] * n[1] for *_x, n in boxes) < stream.SMALL_2D_POINTS
         src, name, block, smem, n_items, geom, sig = codegen.kernel_source_for(
-            plan, rank, dtype, self.skeleton)
+            plan, rank, dtype, self.skeleton, small)
         kern = self.dev.kernel(src, name, block, smem)
         items = []
         for si, ps, tile, lo, n in boxes:

@@ -34,18 +34,18 @@ from .wire import DTYPE_F64
 
 MIN_ZCHUNK = 32
 MAX_RADIUS = 4
-SMEM_BUDGET = 150 * 1024
+SMEM_BUDGET = 220 * 1024
 SMEM_PER_SM = 228 * 1024
 
 
 @dataclass(frozen=True)
 class StreamCfg:
-    """Tile / pipeline shape. Defaults = best of the measured sweeps under
-    sustained (power-capped) load (profiles/r1_stream_sweep.md): 128x8 tiles,
-    2 rows per thread, warp-specialised producer, z-register rotation."""
+    """Tile / pipeline shape. Defaults = best of the measured sweeps
+    (profiles/r1_stream_sweep.md): 128x16 tiles, 4 consecutive rows per
+    thread (source_ws2), warp-specialised TMA producer, register z-columns."""
 
     bx: int = 128           # output columns per CTA
-    by: int = 8             # output rows per CTA
+    by: int = 16            # output rows per CTA
     ty: int = 4             # thread rows; each thread computes by // ty rows
     prefetch: int = 3       # planes in flight beyond the stencil's z window
     persistent: bool = False
@@ -53,6 +53,7 @@ class StreamCfg:
     l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
     ws: bool = True         # warp-specialised: dedicated TMA producer warp, full/empty mbarriers
     zreg: bool = True       # (ws only) pure-z offsets of the thread's own column from registers
+    v2: bool = True         # (ws only) source_ws2: consecutive rows, register y-neighbours, unrolled z
 
 
 def _env_cfg() -> StreamCfg:
@@ -64,15 +65,17 @@ def _env_cfg() -> StreamCfg:
                      zchunk=int(e("EST_STREAM_ZCHUNK", d.zchunk)),
                      l2promo=int(e("EST_STREAM_L2PROMO", d.l2promo)),
                      ws=e("EST_STREAM_WS", "1" if d.ws else "0") == "1",
-                     zreg=e("EST_STREAM_ZREG", "1" if d.zreg else "0") == "1")
+                     zreg=e("EST_STREAM_ZREG", "1" if d.zreg else "0") == "1",
+                     v2=e("EST_STREAM_V2", "1" if d.v2 else "0") == "1")
 
 
 DEFAULT = _env_cfg()
 DEFAULT_2D = StreamCfg(bx=int(os.environ.get("EST_STREAM2D_BX", 128)),
-                       by=int(os.environ.get("EST_STREAM2D_BY", 16)),
+                       by=int(os.environ.get("EST_STREAM2D_BY", 48)),
                        ty=int(os.environ.get("EST_STREAM2D_TY", 4)),
-                       prefetch=int(os.environ.get("EST_STREAM2D_PREFETCH", 3)),
-                       persistent=True, ws=True, zreg=False, l2promo=2)
+                       prefetch=int(os.environ.get("EST_STREAM2D_PREFETCH", 2)),
+                       persistent=True, ws=True, zreg=False, l2promo=2,
+                       v2=os.environ.get("EST_STREAM2D_V2", "1") == "1")
 
 
 def layout(st: StmtSig, dtype: int, cfg: StreamCfg):
@@ -93,12 +96,21 @@ def layout(st: StmtSig, dtype: int, cfg: StreamCfg):
     return slots, off, off + 8 * n_bars + 1024
 
 
-def cfg_for(rank: int) -> StreamCfg:
+# rank-2 boxes below this many points (e.g. the 1024^2 C1 grid) use shorter
+# tiles so the grid still covers every SM
+SMALL_2D_POINTS = 8 << 20
+DEFAULT_2D_SMALL = StreamCfg(bx=128, by=16, ty=4, prefetch=3, persistent=True, ws=True, zreg=False,
+                             l2promo=2, v2=True)
+
+
+def cfg_for(rank: int, small: bool = False) -> StreamCfg:
     """Rank-3 nodes stream along z; rank-2 nodes run the same warp-specialised
     TMA pipeline on a (1, Y, X) view: every item is one (BY+2ry) x (BX+2rx)
     tile, and the persistent grid lets the producer prefetch the NEXT items'
     tiles while the current one is computed."""
-    return DEFAULT if rank == 3 else DEFAULT_2D
+    if rank == 3:
+        return DEFAULT
+    return DEFAULT_2D_SMALL if small else DEFAULT_2D
 
 
 def eligible(stmts, rank: int, dtype: int = DTYPE_F64, cfg: StreamCfg | None = None) -> bool:
@@ -157,7 +169,7 @@ __device__ __forceinline__ void tma_load3(void* dst, const void* tm, int x, int 
 def source(sig: NodeSig, rank: int, cfg: StreamCfg | None = None) -> tuple:
     cfg = cfg or cfg_for(rank)
     if cfg.ws:
-        return source_ws(sig, rank, cfg)
+        return source_ws2(sig, rank, cfg) if cfg.v2 else source_ws(sig, rank, cfg)
     BX, BY, TY = cfg.bx, cfg.by, cfg.ty
     st = sig.stmts[0]
     T = CTYPE[sig.dtype]
@@ -441,6 +453,188 @@ def source_ws(sig: NodeSig, rank: int, cfg: StreamCfg) -> tuple:
     for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
         a(f"    for (int k = nzl; k < nzl + {2 * rz}; ++k) if (lane == 0) mbar_arrive(empty{s} + (fill{s} + k) % {stages});")
         a(f"    fill{s} += nzl + {2 * rz};")
+    a("  }")
+    a("}")
+    src = "\n".join(L) + "\n"
+    return src, "est_stream", (CT + 32, 1, 1), smem, 1, {"slots": slots, "smem": smem, "cfg": cfg}
+
+
+def source_ws2(sig: NodeSig, rank: int, cfg: StreamCfg) -> tuple:
+    """Lower-instruction warp-specialised variant (same TMA rings, barriers
+    and work items as source_ws):
+
+    * each thread owns RPT = BY/TY CONSECUTIVE output rows of one column, so
+      in-plane (dy, 0) operands of its own rows come from registers;
+    * the thread's column of every slot with pure-z / centre operands lives in
+      registers (2rz+1 planes) and the plane loop is unrolled 2rz+1 times so
+      the window rotates by renaming instead of moves;
+    * ring stages / phases are counters, output rows are advanced pointers.
+    Parity: the expression is emitted by codegen._emit_expr exactly as in the
+    other skeletons (one rounded IEEE op per plan instruction)."""
+    BX, BY, TY = cfg.bx, cfg.by, cfg.ty
+    st = sig.stmts[0]
+    T = CTYPE[sig.dtype]
+    elem = ELEM[sig.dtype]
+    q = 16 // elem
+    slots, data_bytes, smem = layout(st, sig.dtype, cfg)
+    n_in = st.arity
+    RPT = BY // TY
+    CT = BX * TY
+    NW = CT // 32
+    assert CT % 32 == 0 and BY % TY == 0
+    loads = [ins for ins in st.instructions if ins[0] == "load"]
+    regs = {s for s in range(n_in) if any(i[1] == s and i[2][1] == 0 and i[2][2] == 0 for i in loads)}
+    Z = {s: 2 * slots[s][0][0] + 1 for s in range(n_in)}
+    U = 1
+    for s in regs:
+        U = U * Z[s] // __import__("math").gcd(U, Z[s])
+    L = []
+    a = L.append
+    a(f'// generated by paper_2512_19851_b200/stream.py — skeleton "stream" (TMA 2.5-D, ws2) {cfg}')
+    a(f"typedef {T} T;")
+    a("struct __align__(64) Tmap { unsigned long long w[16]; };")
+    a(f"struct __align__(64) Params {{ Tmap tm[{n_in}];")
+    a("  unsigned long long out; long long opy, opz, nx, ny, nz, zc, nbx, nby, nzc;")
+    a(f"  long long cx0[{n_in}], cy0[{n_in}], cz0[{n_in}]; }};")
+    L.append(_PTX_HELPERS)
+    a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
+    a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
+    a("__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {")
+    a("  unsigned ok; asm volatile(\"{\\n .reg .pred p;\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\\n\"")
+    a("  \" selp.u32 %0, 1, 0, p;\\n}\" : \"=r\"(ok) : \"r\"(smem_u32(b)), \"r\"(parity) : \"memory\"); return ok; }")
+    a("__device__ __forceinline__ void mbar_wait2(unsigned long long* b, unsigned parity) {")
+    a("  if (!mbar_try(b, parity)) mbar_wait(b, parity); }  // fast first probe, bounded slow path")
+    a(f'extern "C" __global__ void __launch_bounds__({CT + 32})')
+    a("est_stream(const __grid_constant__ Params p) {")
+    a("  extern __shared__ __align__(1024) unsigned char smem[];")
+    a(f"  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + {data_bytes});")
+    a("  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;")
+    a("  const int nbx = (int)p.nbx, nby = (int)p.nby;")
+    a("  const int n_items = nbx * nby * (int)p.nzc;")
+    nb = 0
+    for s_, (_r, _wh, stages, _pl, off) in enumerate(slots):
+        a(f"  unsigned long long* full{s_} = bars + {nb};")
+        a(f"  unsigned long long* empty{s_} = bars + {nb + stages};")
+        nb += 2 * stages
+    a("  if (tid == 0) {")
+    for s_, (_r, _wh, stages, _pl, _off) in enumerate(slots):
+        a(f"    for (int i = 0; i < {stages}; ++i) {{ mbar_init(full{s_} + i, 1); mbar_init(empty{s_} + i, {NW}); }}")
+    a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
+    a("  }")
+    a("  __syncthreads();")
+    # ---------------- producer warp (identical issue order to source_ws)
+    a(f"  if (warp == {NW}) {{")
+    a("    if (lane != 0) return;")
+    for s_ in range(n_in):
+        a(f"    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm[{s_}]) : \"memory\");")
+    for s_ in range(n_in):
+        a(f"    int fill{s_} = 0;")
+    a("    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+    a("      const int bx = item % nbx, rest = item / nbx;")
+    a("      const int by = rest % nby, bzc = rest / nby;")
+    a(f"      const int x0 = bx * {BX}, y0 = by * {BY};")
+    a("      const int zs = bzc * (int)p.zc;")
+    a("      const int nzl = ((zs + (int)p.zc) < (int)p.nz ? (int)p.zc : (int)p.nz - zs);")
+    a("      for (int t = 0; t < nzl; ++t) {")
+    for s_, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
+        a(f"        for (int k = (t == 0 ? 0 : t + {2 * rz}); k <= t + {2 * rz}; ++k) {{")
+        a(f"          const int g = fill{s_} + k, stg = g % {stages};")
+        a(f"          if (g >= {stages}) mbar_wait(empty{s_} + stg, ((g / {stages}) - 1) & 1);")
+        a(f"          const int xs = (int)p.cx0[{s_}] + x0 - {rx};")
+        a(f"          mbar_expect(full{s_} + stg, {w * h * elem});")
+        a(f"          tma_load3(smem + {off} + stg * {plane}, &p.tm[{s_}], xs - (xs & {q - 1}),"
+          f" (int)p.cy0[{s_}] + y0 - {ry}, (int)p.cz0[{s_}] + zs + k - {rz}, full{s_} + stg);")
+        a("        }")
+    a("      }")
+    for s_, ((rz, _ry, _rx), _wh, _stg, _pl, _off) in enumerate(slots):
+        a(f"      fill{s_} += nzl + {2 * rz};")
+    a("    }")
+    a("    return;")
+    a("  }")
+    # ---------------- compute warps
+    a(f"  const int tx = tid % {BX}, ty = tid / {BX};")
+    for s_ in range(n_in):
+        a(f"  int fill{s_} = 0;")
+    for s_ in sorted(regs):
+        a(f"  T {', '.join(f'c{s_}_{r}_{k}' for r in range(RPT) for k in range(Z[s_]))};")
+    a("  const long long opy = p.opy, opz = p.opz;")
+    a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+    a("    const int bx = item % nbx, rest = item / nbx;")
+    a("    const int by = rest % nby, bzc = rest / nby;")
+    a(f"    const int x0 = bx * {BX}, y0 = by * {BY};")
+    a("    const int zs = bzc * (int)p.zc;")
+    a("    const int nzl = ((zs + (int)p.zc) < (int)p.nz ? (int)p.zc : (int)p.nz - zs);")
+    a(f"    const int yr = y0 + ty * {RPT};")
+    a(f"    T* __restrict__ orow = reinterpret_cast<T*>(p.out) + (long long)zs * opz + (long long)yr * opy + (x0 + tx);")
+    a("    const bool colok = (x0 + tx) < (int)p.nx;")
+    for r in range(RPT):
+        a(f"    const bool ok{r} = colok && (yr + {r}) < (int)p.ny;")
+    for s_, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
+        a(f"    const T* base{s_} = reinterpret_cast<const T*>(smem + {off}) + ((((int)p.cx0[{s_}] + x0 - {rx}) & {q - 1})"
+          f" + (ty * {RPT} + {ry}) * {w} + tx + {rx});  // (row 0, dx 0) of this thread, stage 0")
+        a(f"    int st{s_} = fill{s_} % {stages}, ph{s_} = (fill{s_} / {stages}) & 1;  // stage/phase of plane z")
+    a(f"    for (int z0 = 0; z0 < nzl; z0 += {U}) {{")
+    for m in range(U):
+        def col(s_, r, k, m=m):
+            return f"c{s_}_{r}_{(k + m) % Z[s_]}"
+        a(f"      if (z0 + {m} < nzl) {{  // output plane z = z0 + {m}")
+        for s_, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
+            pe = plane // elem
+            # stage of plane index z + d (d = 0 .. 2rz): st + d wrapped
+            a(f"        {{ int sn = st{s_} + {2 * rz}, pn = ph{s_}; if (sn >= {stages}) {{ sn -= {stages}; pn ^= 1; }}")
+            if m == 0:
+                a(f"          if (z0 == 0) {{  // first plane of the item: the whole window")
+                a(f"            for (int d = 0; d < {2 * rz}; ++d) {{ int sd = st{s_} + d, pd = ph{s_};"
+                  f" if (sd >= {stages}) {{ sd -= {stages}; pd ^= 1; }} mbar_wait2(full{s_} + sd, pd); }}")
+                if s_ in regs:
+                    for d in range(2 * rz):
+                        a(f"            {{ int sd = st{s_} + {d}; if (sd >= {stages}) sd -= {stages};")
+                        for r in range(RPT):
+                            a(f"              {col(s_, r, d)} = base{s_}[sd * {pe} + {r * w}];")
+                        a("            }")
+                a("          }")
+            a(f"          mbar_wait2(full{s_} + sn, pn);")
+            if s_ in regs:
+                for r in range(RPT):
+                    a(f"          {col(s_, r, 2 * rz)} = base{s_}[sn * {pe} + {r * w}];")
+            a("        }")
+        need = {}
+        for ins in loads:
+            s_, (dz, dy, dx) = ins[1], ins[2]
+            if s_ in regs and dy == 0 and dx == 0:
+                continue
+            need.setdefault(s_, set()).add(dz)
+        for s_, dzs in sorted(need.items()):
+            (rz, ry, rx), (w, h), stages, plane, off = slots[s_]
+            for dz in sorted(dzs):
+                nm = f"P{s_}_{'m' if dz < 0 else 'p'}{abs(dz)}"
+                a(f"        const T* {nm}; {{ int sd = st{s_} + {rz + dz}; if (sd >= {stages}) sd -= {stages}; {nm} = base{s_} + sd * {plane // elem}; }}")
+        for r in range(RPT):
+            def load(slot, off3, r=r):
+                dz, dy, dx = off3
+                (rz, ry, rx), (w, h), _stg, _pl, _o = slots[slot]
+                if slot in regs and dy == 0 and dx == 0:
+                    return col(slot, r, rz + dz)
+                if slot in regs and dz == 0 and dx == 0 and 0 <= r + dy < RPT:
+                    return col(slot, r + dy, rz)
+                nm = f"P{slot}_{'m' if dz < 0 else 'p'}{abs(dz)}"
+                return f"{nm}[{(r + dy) * w + dx}]"
+            lines, res = _emit_expr(st, sig.dtype, load)
+            a(f"        if (ok{r}) {{")
+            for ln in lines:
+                a("          " + ln)
+            a(f"          orow[{r} * opy] = {res};")
+            a("        }")
+        a("        orow += opz;")
+        a("        __syncwarp();")
+        for s_, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
+            a(f"        if (lane == 0) mbar_arrive(empty{s_} + st{s_});  // plane z of slot {s_} is dead")
+            a(f"        if (++st{s_} == {stages}) {{ st{s_} = 0; ph{s_} ^= 1; }}")
+        a("      }")
+    a("    }")
+    for s_, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
+        a(f"    for (int k = nzl; k < nzl + {2 * rz}; ++k) if (lane == 0) mbar_arrive(empty{s_} + (fill{s_} + k) % {stages});")
+        a(f"    fill{s_} += nzl + {2 * rz};")
     a("  }")
     a("}")
     src = "\n".join(L) + "\n"

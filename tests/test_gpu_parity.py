@@ -224,3 +224,27 @@ def test_stream_multi_slot_mixed_radius(radii):
             assert bits_equal(job.fetch(aid), want[aid]), aid
     finally:
         job.close()
+
+
+def test_large_2d_tiles_bit_exact():
+    """Rank-2 boxes of >= stream.SMALL_2D_POINTS points run the tall-tile
+    configuration (128 x 48, 12 consecutive rows per thread)."""
+    from paper_2512_19851_b200 import stream
+    n = 3072
+    assert (n - 4) ** 2 >= stream.SMALL_2D_POINTS
+    prog = DagProgram()
+    names = wave2d_program(prog, n, 6, dtype=DTYPE_F32)
+    want = reference_execute_dag(prog.dag, prog.shapes, prog.dtypes)
+    job, _ = run_program(prog)
+    try:
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), aid
+    finally:
+        job.close()
+    prog = DagProgram()
+    names = laplace_program(prog, 3000, 5)
+    job, _ = run_program(prog, fused=True)
+    try:
+        assert bits_equal(job.fetch(names["u"]), laplace_reference(3000, 5))
+    finally:
+        job.close()
