@@ -59,6 +59,9 @@ def migrate_tiles(job, plan: dict) -> dict:
 
     Returns stats {tiles_in, tiles_out, bytes_in}.
     """
+    import time
+
+    t0 = time.perf_counter()
     store, dev = job.store, job.dev
     dev.sync()
     # every worker learns the uniform local epochs (a tile-less worker has none)
@@ -90,6 +93,7 @@ def migrate_tiles(job, plan: dict) -> dict:
             tile.local_epoch[a] = epochs.get(a, 0)
             tile.ghost_epoch[a] = epochs.get(a, 0)
     dev.sync()
+    t1 = time.perf_counter()
     job.barrier()  # every pull has completed before anyone frees a departed tile
     for coords in outgoing:
         tile = store.tiles.pop(coords)
@@ -102,8 +106,11 @@ def migrate_tiles(job, plan: dict) -> dict:
         store.bump_local_epoch(a)
         for tile in store.tiles.values():
             tile.ghost_epoch[a] = tile.local_epoch[a] - 1
+    t2 = time.perf_counter()
     job.exchange_buffers()
-    return {"tiles_in": len(incoming), "tiles_out": len(outgoing), "bytes_in": nbytes}
+    return {"tiles_in": len(incoming), "tiles_out": len(outgoing), "bytes_in": nbytes,
+            "pull_ms": round((t1 - t0) * 1e3, 1), "barrier_free_ms": round((t2 - t1) * 1e3, 1),
+            "peer_maps_ms": round((time.perf_counter() - t2) * 1e3, 1)}
 
 
 # --------------------------------------------------------------------------
@@ -116,6 +123,8 @@ def checkpoint_tiles(job, client: DaemonClient, owner: int) -> tuple:
     records = []
     if store is None:
         return records, {}
+    # allocate every blob first, then one batch of D2D copies and ONE sync
+    pending = []
     for coords in sorted(store.tiles):
         tile = store.tiles[coords]
         for a in sorted(store.arrays):
@@ -128,11 +137,13 @@ def checkpoint_tiles(job, client: DaemonClient, owner: int) -> tuple:
             alloc_id, handle = client.dev_alloc(payload, meta)
             dst = dev.ipc_open(handle)
             dev.copy_box(_interior_box(buf, dst, True), buf.elem, COMPUTE)
-            dev.sync()
-            dev.ipc_close(dst)
+            pending.append(dst)
             records.append({"array": a, "tile": list(coords), "owner": owner,
                             "daemon": client.address, "alloc_id": alloc_id,
                             "nbytes": len(header) + payload})
+    dev.sync()
+    for dst in pending:
+        dev.ipc_close(dst)
     arrays_meta = {}
     for a, info in store.arrays.items():
         depth = next((list(t.depths[a]) for t in store.tiles.values()), None)
@@ -188,6 +199,7 @@ def restore_tiles(job, manifest: dict) -> dict:
         store.arrays[a] = ArrayInfo(a, tuple(meta["shape"]), int(meta.get("dtype", 0)))
         depths[a] = tuple(meta["depth"])
     clients: dict = {}
+    opened = []  # (client, alloc id, mapped address): all copies in flight, ONE sync
     try:
         for rec in manifest["allocations"]:
             if rec["owner"] != job.rank:
@@ -204,14 +216,16 @@ def restore_tiles(job, manifest: dict) -> dict:
             tile = store.tiles.setdefault(tuple(coords), GpuTile(tuple(coords)))
             buf = TileBuffer(dev, ext, depth, int(meta.get("dtype", 0)))
             src = dev.ipc_open(handle)
+            opened.append((cl, rec["alloc_id"], src))
             dev.copy_box(_interior_box(buf, src, False), buf.elem, COMPUTE)
-            dev.sync()
-            dev.ipc_close(src)
-            cl.dev_free(rec["alloc_id"])
             tile.buffers[a] = buf
             tile.depths[a] = tuple(depth)
             tile.local_epoch[a] = epoch
             tile.ghost_epoch[a] = epoch
+        dev.sync()
+        for cl, alloc_id, src in opened:
+            dev.ipc_close(src)
+            cl.dev_free(alloc_id)
     finally:
         for cl in clients.values():
             cl.close()

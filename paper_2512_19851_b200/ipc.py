@@ -72,8 +72,9 @@ class IpcPeerTransport(LocalPeerTransport):
         self.readers: dict = {}
         self.pull_launches = 0
         self.peer_events: dict = {}
-        self.peer_maps: dict = {}      # (owner, coords, array) -> (layout TileBuffer, addr)
-        self.opened: list = []
+        self.peer_maps: dict = {}      # (owner, coords, array) -> (layout TileBuffer, addr, handle)
+        self.peer_tables: dict = {}    # (owner, coords, array) -> (handle, ext, depth, dtype)
+        self.peer_event_handles: dict = {}
         self.spin_s = 0.0
         self.peer_version = 0
         self._pulls: dict = {}
@@ -84,47 +85,95 @@ class IpcPeerTransport(LocalPeerTransport):
                 "pulled": [e.ipc_handle() for e in self.pulled]}
 
     def open_peer_events(self, table: dict) -> None:
-        for owner, handles in table.items():
-            if owner == self.w:
-                continue
-            self.peer_events[owner] = {k: [self.dev.open_event(h) for h in v]
-                                       for k, v in handles.items()}
+        """Remember the peers' event handles; each is opened on first use
+        (only halo neighbours ever wait on each other's events)."""
+        self.peer_event_handles = {o: h for o, h in table.items() if o != self.w}
 
     def buffer_table(self) -> dict:
         out = {}
         for coords, tile in self.store.tiles.items():
             for array, buf in tile.buffers.items():
                 out[(tuple(coords), array)] = (self.dev.ipc_handle(buf.ptr), buf.ext[3 - buf.rank:],
-                                               buf.depth[3 - buf.rank:], buf.dtype)
+                                               buf.depth[3 - buf.rank:], buf.dtype, buf.serial)
         return out
 
     def open_peer_buffers(self, tables: list) -> None:
-        self.close_peer_buffers()
+        """Install the peers' buffer handle tables. Mappings are opened lazily
+        (`peer_buffer`): a worker maps only the tiles it actually reads
+        (halo neighbours, migration sources). A mapping whose handle is
+        unchanged survives; changed / departed buffers are unmapped."""
         self.peer_version += 1
+        wanted = {}
         for owner, table in enumerate(tables):
             if owner == self.w:
                 continue
-            for (coords, array), (handle, ext, depth, dtype) in table.items():
-                addr = self.dev.ipc_open(handle)
-                self.opened.append(addr)
-                layout = TileBuffer(self.dev, ext, depth, dtype, ptr=addr)
-                self.peer_maps[(owner, coords, array)] = (layout, addr)
+            for (coords, array), entry in table.items():
+                wanted[(owner, tuple(coords), array)] = entry
+        for key, (layout, addr, handle) in list(self.peer_maps.items()):
+            ent = wanted.get(key)
+            if ent is None or (ent[0], ent[4]) != handle:
+                try:
+                    self.dev.ipc_close(addr)
+                except Exception:
+                    pass
+                del self.peer_maps[key]
+        self.peer_tables = wanted
+
+    def map_neighbours(self) -> int:
+        """Open, now, the mappings / events halo rounds will use: every array
+        of every remote tile adjacent to an owned tile (a bounded set, unlike
+        the full table). Returns the number of mappings opened."""
+        from .exchange import N, E, W, neighbour
+
+        before = len(self.peer_maps)
+        owners = self.job.owner_map or {}
+        peers = set()
+        for coords in self.store.tiles:
+            for a, info in self.store.arrays.items():
+                dirs = (E, W) if info.rank != 2 else range(N, N + 8)
+                for d in dirs:
+                    nb = neighbour(self.store.decomp, info.rank, coords, d)
+                    if nb is None or owners.get(nb, self.w) == self.w:
+                        continue
+                    key = (owners[nb], tuple(nb), a)
+                    if key in self.peer_tables:
+                        self.peer_buffer(*key)
+                        peers.add(owners[nb])
+        for p in peers:
+            for kind in ("ready", "pulled"):
+                for slot in range(len(self.peer_event_handles.get(p, {}).get(kind, []))):
+                    self.peer_event(p, kind, slot)
+        return len(self.peer_maps) - before
 
     def close_peer_buffers(self) -> None:
-        for addr in self.opened:
+        for _layout, addr, _h in self.peer_maps.values():
             try:
                 self.dev.ipc_close(addr)
             except Exception:
                 pass
-        self.opened.clear()
         self.peer_maps.clear()
+        self.peer_tables = {}
 
     # -- protocol hooks ----------------------------------------------------------
     def peer_buffer(self, owner: int, coords, array: int):
-        return self.peer_maps[(owner, tuple(coords), array)]
+        key = (owner, tuple(coords), array)
+        hit = self.peer_maps.get(key)
+        if hit is None:
+            handle, ext, depth, dtype, serial = self.peer_tables[key]
+            addr = self.dev.ipc_open(handle)
+            layout = TileBuffer(self.dev, ext, depth, dtype, ptr=addr)
+            hit = self.peer_maps[key] = (layout, addr, (handle, serial))
+        return hit[0], hit[1]
 
     def peer_event(self, owner: int, kind: str, slot: int):
-        return self.peer_events[owner][kind][slot]
+        evs = self.peer_events.setdefault(owner, {})
+        lst = evs.get(kind)
+        if lst is None:
+            lst = evs[kind] = [None] * len(self.peer_event_handles[owner][kind])
+        ev = lst[slot]
+        if ev is None:
+            ev = lst[slot] = self.dev.open_event(self.peer_event_handles[owner][kind][slot])
+        return ev
 
     def wait_seq(self, owner: int, kind: str, r: int) -> None:
         row = 0 if kind == "ready" else 1
@@ -161,7 +210,8 @@ class IpcPeerTransport(LocalPeerTransport):
         for evs in self.peer_events.values():
             for lst in evs.values():
                 for e in lst:
-                    e.close()
+                    if e is not None:
+                        e.close()
         for e in self.ready + self.pulled:
             e.close()
 
@@ -176,7 +226,7 @@ class IpcGpuJob:
 
     def __init__(self, rank: int, world: int, device: int = 0, odf: int = 1,
                  skeleton: str = "auto", group=None, timeout_s: float = 600.0,
-                 decomp=None, owner_map: dict | None = None):
+                 decomp=None, owner_map: dict | None = None, dev: Device | None = None):
         if group is None:
             import torch.distributed as dist
 
@@ -188,7 +238,7 @@ class IpcGpuJob:
         self.group = group
         self.rank, self.world, self.odf = rank, world, odf
         self.timeout_s = timeout_s
-        self.dev = Device(device)
+        self.dev = dev if dev is not None else Device(device)  # a worker may pre-create it
         self.devs = [self.dev]
         self.skeleton = skeleton
         self.decomp = decomp
@@ -232,6 +282,7 @@ class IpcGpuJob:
         self.dev.sync()
         tables = self._all_gather(self.transport.buffer_table())
         self.transport.open_peer_buffers(tables)
+        self.transport.map_neighbours()
         self.barrier()
 
     @property

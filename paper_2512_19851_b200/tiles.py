@@ -119,7 +119,8 @@ class TileBuffer:
     """One padded device buffer (see module docstring for the layout)."""
 
     __slots__ = ("dev", "ptr", "rank", "dtype", "elem", "ext", "depth", "xoff", "py", "pz",
-                 "nz", "nbytes", "owned")
+                 "nz", "nbytes", "owned", "serial")
+    _serials = __import__("itertools").count(1)
 
     def __init__(self, dev: Device, ext, depth, dtype: int, ptr: int | None = None):
         self.dev = dev
@@ -136,6 +137,7 @@ class TileBuffer:
         self.nbytes = self.pz * self.nz * self.elem
         self.owned = ptr is None
         self.ptr = dev.alloc(self.nbytes) if ptr is None else ptr
+        self.serial = next(TileBuffer._serials)  # identifies this allocation in peer tables
 
     @staticmethod
     def layout_bytes(ext, depth, dtype: int) -> int:

@@ -55,6 +55,14 @@ class GpuWorker:
         self.listener.listen(64)
         self.address = "127.0.0.1:%d" % self.listener.getsockname()[1]
         host, port = coordinator.rsplit(":", 1)
+        # CUDA context + libest BEFORE registering: a (re)spawned worker is
+        # device-ready when the coordinator's restart stage sees it
+        # (coordinator.py:562-579), so W_RESTORE is pure data movement
+        self._dev = None
+        self._dev_err = None
+        self._dev_thread = threading.Thread(target=self._make_device, daemon=True)
+        self._dev_thread.start()
+        self._dev_thread.join()
         self.coord = socket.create_connection((host, int(port)))
         self.coord.setsockopt(socket.IPPROTO_TCP, socket.TCP_NODELAY, 1)
         send_json(self.coord, REGISTER, {"role": "worker", "id": self.id, "address": self.address})
@@ -98,11 +106,28 @@ class GpuWorker:
                 self._pending_socks.clear()
         return self.group
 
+    def _make_device(self) -> None:
+        try:
+            from .device import Device
+
+            self._dev = Device(self.device)
+        except BaseException as exc:  # surfaced by the first command that needs it
+            self._dev_err = exc
+
+    def _device(self):
+        self._dev_thread.join()
+        if self._dev_err is not None:
+            raise self._dev_err
+        dev, self._dev = self._dev, None  # handed to the job, which owns and closes it
+        dev.sync()  # makes the device current on THIS thread too (ctx-less calls: IPC, pinned memory)
+        return dev
+
     def _new_job(self, decomp, owners):
         from .ipc import IpcGpuJob
 
+        dev = self._device() if self._dev is not None or self._dev_err else None
         return IpcGpuJob(self.id, len(self.peer_dir), device=self.device, group=self._ensure_group(),
-                         decomp=decomp, owner_map=owners)
+                         decomp=decomp, owner_map=owners, dev=dev)
 
     # -- control loop (worker.py:252-294) ----------------------------------------
     def run(self) -> None:
@@ -209,6 +234,7 @@ class GpuWorker:
     def _handle_restore(self, meta: dict) -> None:
         from .elastic import decomp_from_manifest, owner_map_from_manifest, read_manifest, restore_tiles
 
+        t0 = time.perf_counter()
         manifest = read_manifest(meta["path"])
         self.worker_count = meta["worker_count"]
         decomp = decomp_from_manifest(manifest)
@@ -217,13 +243,17 @@ class GpuWorker:
             send_json(self.coord, REPLY_OK, {})
             return
         self.job = self._new_job(decomp, owner_map_from_manifest(manifest))
+        t1 = time.perf_counter()
         depths = restore_tiles(self.job, manifest)
+        t2 = time.perf_counter()
         self.job.executor.depths = depths
         for a, info in self.job.store.arrays.items():
             self.job.shapes[a] = info.shape
             self.job.dtypes[a] = info.dtype
             self.job._next = max(self.job._next, a + 1)
         self.job.exchange_buffers()
+        log.info("restore: job %.1f ms, copies %.1f ms, peer maps %.1f ms", (t1 - t0) * 1e3,
+                 (t2 - t1) * 1e3, (time.perf_counter() - t2) * 1e3)
         send_json(self.coord, REPLY_OK, {})
 
     def shutdown(self) -> None:

@@ -49,7 +49,7 @@ def main(argv=None):
     lups = (n - 2) ** 2 * it
     rows = sorted({1, n // 4 - 1, n // 4, n // 2 - 1, n // 2, n // 2 + 1, 3 * n // 4, n - 2})
     phases, rescales = {}, []
-    with GpuLauncher(workers=w, max_workers=w, odf=1) as job:
+    with GpuLauncher(workers=w, max_workers=w, odf=1, scratch=os.environ.get("EST_SCRATCH")) as job:
         sess = client.Session(job.client_endpoint, timeout=1800)
         bs = client.BatchingSession(sess, flush_depth=args.flush)
         try:
