@@ -86,9 +86,34 @@ def standard_sources() -> list:
     return sorted(srcs)
 
 
+def install_reference(src: str = "/root/reference/pkg") -> str | None:
+    """Best effort: the unmodified reference into baseline/_ref (git-ignored;
+    used by the integration tests and the C5 rescale bench). Offline pip from
+    a copy, since /root/reference is read-only."""
+    import shutil
+    import tempfile
+
+    dst = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(dst, "elastencil")) or not os.path.isdir(src):
+        return dst if os.path.isdir(dst) else None
+    tmp = tempfile.mkdtemp(prefix="refpkg-")
+    try:
+        shutil.copytree(src, os.path.join(tmp, "pkg"))
+        subprocess.run([sys.executable, "-m", "pip", "install", "--no-index", "--no-build-isolation",
+                        "--no-deps", "--target", dst, os.path.join(tmp, "pkg")],
+                       check=True, capture_output=True)
+        return dst
+    except (OSError, subprocess.CalledProcessError) as exc:
+        print(f"[build] reference install skipped: {exc}", file=sys.stderr)
+        return None
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
 def build_all(prebuild: bool = True) -> None:
     build_libest()
     build_oracle()
+    install_reference()
     if prebuild:
         new, cached = precompile_sources(standard_sources())
         print(f"[build] kernel cache: {new} compiled, {cached} already cached", file=sys.stderr)
