@@ -80,6 +80,8 @@ def bytes_per_launch(w, tag) -> int:
     sweeps (temporal.py) reads the input array once and writes each of the two
     arrays once: elem * (N_in + 2 * N_out)."""
     kind, sweeps = tag
+    if kind == "res":  # resident chain: every sweep is a full pass (in L2)
+        return bytes_per_iter(w) * sweeps
     if kind != "tb":
         return bytes_per_iter(w)
     n = w["n"]
@@ -379,11 +381,18 @@ def main():
 
     # ---- roofline ------------------------------------------------------------
     peak, peak_src = load_peaks()
+    # work done by the dominant kind = the sweeps it covered in the timed
+    # steps (a node may be split into interior/boundary launches, a temporal
+    # chain covers K nodes), so achieved = covered bytes / summed kernel time
     sweeps = dom[1]
-    mean_k = statistics.mean(kt) if kt else dev_ms / max(1, args.steps * w["iters_per_step"])
+    ev_steps = args.steps if inline_timing else 2
+    tb_sweeps = sum(len(v) * k for (kind, k), v in by_tag.items() if kind in ("tb", "res"))
+    covered = len(kt) * sweeps if dom[0] in ("tb", "res") else ev_steps * w["iters_per_step"] - tb_sweeps
+    logical_launches = max(1, covered // sweeps)
     bytes_launch = bytes_per_launch(w, dom)
     if world > 1:
         bytes_launch //= world
+    mean_k = (sum(kt) / logical_launches) if kt else dev_ms / max(1, args.steps * w["iters_per_step"])
     achieved = bytes_launch / (mean_k / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -408,7 +417,8 @@ def main():
                    "kernel_timing": "inline" if inline_timing else "separate 2-step pass (graphs in timed region)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "est_tb (K=%d fused sweeps)" % sweeps if dom[0] == "tb" else "est_stream/est_node (1 sweep)",
+                     "kernel": {"tb": "est_tb (K=%d fused sweeps)" % sweeps,
+                                "res": "est_resident (%d sweeps)" % sweeps}.get(dom[0], "est_stream/est_node (1 sweep)"),
                      "sweeps_per_launch": sweeps,
                      "kernel_ms": mean_k, "bytes_per_launch": bytes_launch,
                      "peak_source": peak_src,

@@ -77,6 +77,12 @@ def standard_sources() -> list:
                     srcs.add(kernel_source_for(plan, rank, dt, skel)[0])
                 if rank == 2:
                     srcs.add(kernel_source_for(plan, rank, dt, "auto", small=True)[0])
+                if rank in (2, 3) and len(plan.statements) == 1:
+                    from . import resident
+                    from .codegen import stmt_sig as _ss
+                    rs = _ss(plan.statements[0], rank)
+                    if resident.eligible(rs, dt, rank):
+                        srcs.add(resident.source(rs, dt, rank)[0])
                 if rank == 3 and len(plan.statements) == 1:
                     from . import temporal
                     from .codegen import stmt_sig

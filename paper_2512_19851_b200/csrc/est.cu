@@ -71,6 +71,7 @@ struct Driver {
     decltype(&cuModuleUnload) moduleUnload = nullptr;
     decltype(&cuLaunchKernel) launchKernel = nullptr;
     decltype(&cuFuncSetAttribute) funcSetAttribute = nullptr;
+    decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) occupancy = nullptr;
     bool ok = false;
 };
 static Driver g_drv;
@@ -97,6 +98,7 @@ static int driver() {
     rc |= resolve("cuLaunchKernel", g_drv.launchKernel);
     rc |= resolve("cuFuncSetAttribute", g_drv.funcSetAttribute);
     rc |= resolve("cuTensorMapEncodeTiled", g_drv.tensorMapEncodeTiled);
+    rc |= resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", g_drv.occupancy);
     if (rc) return 1;
     g_drv.ok = true;
     return 0;
@@ -469,6 +471,13 @@ extern "C" int est_kernel_set_smem(uint64_t fn, int bytes) {
     if (driver()) return 1;
     CU_TRY(g_drv.funcSetAttribute((CUfunction)(uintptr_t)fn,
                                   CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, bytes));
+    return 0;
+}
+
+extern "C" int est_kernel_occupancy(uint64_t fn, int block, int smem, int *blocks_per_sm) {
+    *blocks_per_sm = 0;
+    if (driver()) return 1;
+    CU_TRY(g_drv.occupancy(blocks_per_sm, (CUfunction)(uintptr_t)fn, block, (size_t)smem));
     return 0;
 }
 

@@ -187,6 +187,13 @@ class Device:
         self._kernels[key] = k
         return k
 
+    def occupancy(self, k: Kernel) -> int:
+        """Co-resident CTAs per SM for k's block shape and shared memory."""
+        n = C.c_int(0)
+        check(self.lib.est_kernel_occupancy(k.fn, int(k.block[0] * k.block[1] * k.block[2]), k.smem,
+                                            C.byref(n)))
+        return n.value
+
     def launch(self, k: Kernel, grid, params: bytes, stream: int = COMPUTE) -> None:
         g = (C.c_uint32 * 3)(*grid)
         b = (C.c_uint32 * 3)(*k.block)

@@ -26,7 +26,7 @@ from __future__ import annotations
 import time
 from dataclasses import dataclass, field
 
-from . import codegen, stream, temporal
+from . import codegen, resident, stream, temporal
 from .analysis import analyze_dag, compile_plan
 from .device import COMPUTE
 from .errors import MalformedDag
@@ -84,6 +84,8 @@ class GpuExecutor:
         self._replay: dict = {}
         self.replays = 0
         self.temporal = temporal.ENABLED  # fuse ping-pong sweep chains (temporal.py)
+        self.resident = resident.ENABLED  # whole L2-resident chains in one launch (resident.py)
+        self._bar = 0                     # grid-barrier counter of the resident skeleton
         self.tb_cfg = temporal.DEFAULT
         self._scratch: dict = {}     # array -> twin TileBuffer for temporal chains
         self._tb_sched: dict = {}
@@ -242,6 +244,9 @@ class GpuExecutor:
                 ent["graph"].close()
         self._replay.clear()
         self.release_scratch()
+        if self._bar:
+            self.dev.free(self._bar)
+            self._bar = 0
 
     # -- execution (executor.py:258-348) ------------------------------------
     def _execute(self, dag, key: bytes | None = None) -> BatchStats:
@@ -274,6 +279,8 @@ class GpuExecutor:
                 # tile without transport has no device work between sweeps)
                 if chain[0] == "lead":
                     self._launch_tb(node, plan, chain[1], key)
+                elif chain[0] == "res":
+                    self._launch_resident(node, plan, chain[1], key)
             elif pending and set(pending) & set(meta.array_max_offset) and self.overlap_eligible(plan):
                 # halo/compute overlap: planes that read no ghost cells go first,
                 # the deferred peer pull runs on the copy lane meanwhile, the
@@ -307,7 +314,10 @@ class GpuExecutor:
         return stats
 
     # -- temporal blocking (temporal.py) ----------------
-    def _tb_candidate(self, plan):
+    def _chain_candidate(self, plan):
+        """(A, B, output bounds, plan instructions, rank, dtype) for a node that
+        can be part of a ping-pong chain: one statement, one input array of the
+        output's shape, type and buffer layout; else None."""
         if len(plan.statements) != 1:
             return None
         ps = plan.statements[0]
@@ -315,34 +325,42 @@ class GpuExecutor:
             return None
         a, b = ps.inputs[0], ps.output
         ia, ib = self.store.arrays.get(a), self.store.arrays.get(b)
-        if ia is None or ib is None or ia.rank != 3 or ia.shape != ib.shape or ia.dtype != ib.dtype:
+        if ia is None or ib is None or ia.rank not in (2, 3) or ia.shape != ib.shape or ia.dtype != ib.dtype:
             return None
         tile = next(iter(self.store.tiles.values()))
         ba, bb = tile.buffers[a], tile.buffers[b]
         if (ba.depth, ba.py, ba.pz, ba.xoff) != (bb.depth, bb.py, bb.pz, bb.xoff):
             return None
-        sig = codegen.stmt_sig(ps, 3)
-        if not temporal.eligible(sig, ia.dtype, self.tb_cfg):
+        return (a, b, tuple(ps.output_slice_bounds), ps.instructions, ia.rank, ia.dtype)
+
+    def _tb_candidate(self, plan):
+        c = self._chain_candidate(plan)
+        if c is None or c[4] != 3:
             return None
-        return (a, b, tuple(ps.output_slice_bounds), ps.instructions)
+        sig = codegen.stmt_sig(plan.statements[0], 3)
+        return c if temporal.eligible(sig, c[5], self.tb_cfg) else None
 
     def temporal_schedule(self, dag, plans, key=None) -> dict:
-        """node id -> ("lead", chain index in its run) | ("member",).
+        """node id -> ("res", sweeps) | ("lead", chain index in its run) | ("member",).
 
         Runs of consecutive candidate nodes that ping-pong A -> B -> A with the
-        same statement and output slice are cut into chains of K nodes; the
-        number of chains per run is kept even so A ends in its own buffer.
-        Only for one tile per job without transport (no exchange between
-        sweeps); everything else runs node by node."""
-        if (not self.temporal or self.transport is not None or len(self.store.tiles) != 1
-                or self.store.decomp.n_tiles != 1 or self.skeleton not in ("auto", "tb")):
+        same statement and output slice: if both arrays fit in L2 the whole
+        run is one resident launch (resident.py); otherwise, with temporal
+        chains enabled, the run is cut into chains of K nodes (temporal.py),
+        the number of chains kept even so A ends in its own buffer. Only for
+        one tile per job without transport (no exchange between sweeps);
+        everything else runs node by node."""
+        if (not (self.temporal or self.resident) or self.transport is not None
+                or len(self.store.tiles) != 1 or self.store.decomp.n_tiles != 1
+                or self.skeleton not in ("auto", "tb")):
             return {}
-        ck = (key, self.store.version, self.tb_cfg) if key is not None else None
+        ck = (key, self.store.version, self.tb_cfg, self.temporal, self.resident) if key is not None else None
         hit = self._tb_sched.get(ck) if ck is not None else None
         if hit is not None:
             return hit
         K = self.tb_cfg.k
-        cand = [self._tb_candidate(p) for p in plans]
+        cand = [self._chain_candidate(p) for p in plans]
+        tile = next(iter(self.store.tiles.values()))
         sched: dict = {}
         i, n = 0, len(cand)
         while i < n:
@@ -354,19 +372,68 @@ class GpuExecutor:
             while (j < n and cand[j] is not None and cand[j][2:] == c[2:]
                    and cand[j][0] == cand[j - 1][1] and cand[j][1] == cand[j - 1][0]):
                 j += 1
-            m = (j - i) // K
-            m -= m % 2
-            for ch in range(m):
-                lead = i + ch * K
-                sched[dag.nodes[lead].node_id] = ("lead", ch)
-                for q in range(1, K):
-                    sched[dag.nodes[lead + q].node_id] = ("member",)
+            sig = codegen.stmt_sig(plans[i].statements[0], c[4])
+            if (self.resident and j - i >= 2 and resident.eligible(sig, c[5], c[4])
+                    and resident.fits_l2(tile.buffers[c[0]])):
+                sched[dag.nodes[i].node_id] = ("res", j - i)
+                for q in range(i + 1, j):
+                    sched[dag.nodes[q].node_id] = ("member",)
+            elif self.temporal and c[4] == 3 and temporal.eligible(sig, c[5], self.tb_cfg):
+                m = (j - i) // K
+                m -= m % 2
+                for ch in range(m):
+                    lead = i + ch * K
+                    sched[dag.nodes[lead].node_id] = ("lead", ch)
+                    for q in range(1, K):
+                        sched[dag.nodes[lead + q].node_id] = ("member",)
             i = j
         if ck is not None:
             if len(self._tb_sched) > 256:
                 self._tb_sched.clear()
             self._tb_sched[ck] = sched
         return sched
+
+    def _launch_resident(self, node, plan, sweeps: int, key) -> None:
+        """One persistent launch running `sweeps` ping-pong sweeps in L2."""
+        ps = plan.statements[0]
+        a, b = ps.inputs[0], ps.output
+        tile = next(iter(self.store.tiles.values()))
+        ba, bb = tile.buffers[a], tile.buffers[b]
+        info = self.store.arrays[a]
+        if not self._bar:
+            self._bar = self.dev.alloc(256)
+        self.dev.memset_zero(self._bar, 4, COMPUTE)
+        ck = (key, node.node_id, self.store.version, "res") if key is not None else None
+        rec = self._launches.get(ck) if ck is not None else None
+        if rec is not None and not self.time_kernels:
+            for kern, grid, params in rec:
+                self.dev.launch(kern, grid, params, COMPUTE)
+            return
+        sig = codegen.stmt_sig(ps, info.rank)
+        src, name, block, smem, geo = resident.source(sig, info.dtype, info.rank)
+        kern = self.dev.kernel(src, name, block, 0)
+        d = (0,) * (3 - info.rank) + tuple(ba.depth[3 - info.rank:])
+        bounds = ((0, 1),) * (3 - info.rank) + tuple(ps.output_slice_bounds)
+        s_lo = tuple(lo + dd for (lo, _), dd in zip(bounds, d))
+        s_hi = tuple(hi + dd for (_, hi), dd in zip(bounds, d))
+        org = ba.xoff * ba.elem
+        params = resident.pack_params(ba.ptr + org, bb.ptr + org, self._bar, ba, s_lo, s_hi, sweeps, geo)
+        # every CTA must be co-resident (grid barrier): size by measured occupancy
+        occ = self.dev.occupancy(kern)
+        if occ < 1:
+            raise RuntimeError("resident chain kernel cannot be resident on this device")
+        cfg = geo["cfg"]
+        n_tiles = 1
+        for lo, hi, t in zip(s_lo, s_hi, (cfg.tz, cfg.ty, cfg.tx)):
+            n_tiles *= -(-(hi - lo) // t)
+        grid = (max(1, min(self.dev.sm_count * min(geo["min_blocks"], occ), n_tiles)), 1, 1)
+        self._recording = [] if ck is not None else None
+        try:
+            self._launch(kern, grid, params, tag=("res", sweeps))
+        finally:
+            rec, self._recording = self._recording, None
+        if ck is not None and rec is not None:
+            self._launches[ck] = rec
 
     def _scratch_for(self, array: int, buf):
         tw = self._scratch.get(array)

@@ -93,6 +93,9 @@ class FakeDevice:
     def kernel(self, src, name, block, smem=0):
         return FakeKernel(name, block, smem)
 
+    def occupancy(self, k):
+        return 8
+
     def launch(self, k, grid, params, stream=0):
         self.launches += 1
         self.log.append(("launch", grid[0], getattr(k, "name", "")))

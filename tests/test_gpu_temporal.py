@@ -1,6 +1,8 @@
-"""GPU parity of the temporal-blocking skeleton (temporal.py): K fused
-ping-pong sweeps must be bit-identical to the oracle (fp64; fp32 within the
-north star's 1e-5, in fact bit-identical because the plan order is kept).
+"""GPU parity of the fused-chain skeletons: temporal.py (K fused ping-pong
+sweeps with a twin buffer) and resident.py (a whole L2-resident run in one
+persistent launch with grid barriers). Both must be bit-identical to the
+oracle (fp64; fp32 within the north star's 1e-5, in fact bit-identical
+because the plan order is kept). Every test runs in both modes.
 
 Cases cover partial tiles, output slices that are not the full interior, a
 radius-2 and an asymmetric stencil, odd iteration counts (a leftover sweep on
@@ -19,10 +21,17 @@ from paper_2512_19851_b200.wire import DTYPE_F32, encode_dag
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def _chains_on(monkeypatch):
-    from paper_2512_19851_b200 import temporal
-    monkeypatch.setattr(temporal, "ENABLED", True)
+@pytest.fixture(autouse=True, params=["tb", "resident"])
+def mode(request, monkeypatch):
+    from paper_2512_19851_b200 import resident, temporal
+    monkeypatch.setattr(temporal, "ENABLED", request.param == "tb")
+    monkeypatch.setattr(resident, "ENABLED", request.param == "resident")
+    return request.param
+
+
+def _ran(job, mode) -> bool:
+    ex = job.executors[0]
+    return bool(ex._scratch) if mode == "tb" else bool(ex._bar)
 
 
 def _tb_launches(stats) -> int:
@@ -30,13 +39,13 @@ def _tb_launches(stats) -> int:
 
 
 @pytest.mark.parametrize("n,iters", [(24, 4), (40, 8), (67, 6), (64, 13), (130, 4)])
-def test_heat3d_chains_bit_exact(n, iters):
+def test_heat3d_chains_bit_exact(n, iters, mode):
     prog = DagProgram()
     heat3d_program(prog, n, iters, seed_fills=12)
     want = strict_execute_dag(prog.dag, prog.shapes)
     job, stats = run_program(prog, fused=True)
     try:
-        assert job.executors[0]._scratch, "temporal chain did not run"
+        assert _ran(job, mode), "fused chain did not run"
         for aid in prog.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), (n, iters, aid)
     finally:
@@ -62,7 +71,7 @@ def _star(u, box, radius=1, axes=(0, 1, 2)):
     (((2, 38), (2, 38), (2, 38)), 2),     # radius-2 star (depth 2)
     (((3, 30), (5, 33), (2, 38)), 2),
 ])
-def test_subbox_chains_bit_exact(box, radius):
+def test_subbox_chains_bit_exact(box, radius, mode):
     n = 40
     prog = DagProgram()
     u1, u2 = heat3d_setup(prog, n, seed_fills=10)
@@ -72,14 +81,14 @@ def test_subbox_chains_bit_exact(box, radius):
     want = reference_execute_dag(prog.dag, prog.shapes)
     job, _ = run_program(prog)
     try:
-        assert job.executors[0]._scratch
+        assert _ran(job, mode)
         for aid in prog.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), (box, radius, aid)
     finally:
         job.close()
 
 
-def test_asymmetric_offsets_bit_exact():
+def test_asymmetric_offsets_bit_exact(mode):
     """Asymmetric z-star stencil (dz in {-2, 1}, in-plane (1,-1) and (-1,0))."""
     n = 36
     prog = DagProgram()
@@ -97,20 +106,20 @@ def test_asymmetric_offsets_bit_exact():
     want = reference_execute_dag(prog.dag, prog.shapes)
     job, _ = run_program(prog)
     try:
-        assert job.executors[0]._scratch
+        assert _ran(job, mode)
         for aid in prog.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), aid
     finally:
         job.close()
 
 
-def test_heat3d_fp32_chains():
+def test_heat3d_fp32_chains(mode):
     prog = DagProgram()
     heat3d_program(prog, 48, 8, seed_fills=10, dtype=DTYPE_F32)
     want = reference_execute_dag(prog.dag, prog.shapes, prog.dtypes)
     job, _ = run_program(prog)
     try:
-        assert job.executors[0]._scratch
+        assert _ran(job, mode)
         for aid in prog.shapes:
             got = job.fetch(aid)
             assert got.dtype == np.float32
@@ -120,7 +129,7 @@ def test_heat3d_fp32_chains():
         job.close()
 
 
-def test_repeated_batches_graph_replay_bit_exact():
+def test_repeated_batches_graph_replay_bit_exact(mode):
     """Steady-state batches replay a captured CUDA graph holding the chain kernels."""
     n, per, batches = 48, 10, 5
     setup = DagProgram()
@@ -145,13 +154,14 @@ def test_repeated_batches_graph_replay_bit_exact():
         job.run(setup.dag)
         stats = [job.run_bytes(blob) for _ in range(batches)]
         assert job.executors[0].replays >= 2
-        # 10 sweeps = 4 chains of 2 (chain count kept even) + 2 single sweeps
-        assert stats[1][0].gpu_launches == 4 + 2 + 1
+        # tb: 10 sweeps = 4 chains of 2 (chain count kept even) + 2 single sweeps
+        # + the complement copy; resident: the whole batch is one launch
+        assert stats[1][0].gpu_launches == (4 + 2 + 1 if mode == "tb" else 1)
         for aid in setup.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), aid
 
 
-def test_chain_disabled_equals_enabled():
+def test_chain_disabled_equals_enabled(mode):
     prog = DagProgram()
     heat3d_program(prog, 56, 8, seed_fills=12)
     outs = []
@@ -161,10 +171,11 @@ def test_chain_disabled_equals_enabled():
         try:
             for aid in sorted(prog.shapes):
                 job.create_array(prog.shapes[aid])
-            job.executors[0].temporal = on
+            job.executors[0].temporal = on and mode == "tb"
+            job.executors[0].resident = on and mode == "resident"
             job_stats = job.run(prog.dag)
             outs.append([job.fetch(a) for a in sorted(prog.shapes)])
-            assert bool(job.executors[0]._scratch) == on
+            assert _ran(job, mode) == on
         finally:
             job.close()
         assert job_stats[0].kernel_launches == len(prog.dag.nodes)
@@ -172,8 +183,9 @@ def test_chain_disabled_equals_enabled():
         assert bits_equal(x, y)
 
 
-def test_non_z_star_chain_runs_node_by_node():
-    """A diagonal (dz, dx) load is not chainable: no twin, still bit-exact."""
+def test_non_z_star_chain(mode):
+    """A diagonal (dz, dx) load: not chainable by tb (no twin), resident runs
+    it; bit-exact either way."""
     n = 32
     prog = DagProgram()
     u1, u2 = heat3d_setup(prog, n, seed_fills=6)
@@ -187,8 +199,34 @@ def test_non_z_star_chain_runs_node_by_node():
     want = reference_execute_dag(prog.dag, prog.shapes)
     job, _ = run_program(prog)
     try:
-        assert not job.executors[0]._scratch
+        assert _ran(job, mode) == (mode == "resident")
         for aid in prog.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), aid
+    finally:
+        job.close()
+
+
+def test_resident_2d_laplace_and_wave_sizes(mode):
+    """2-D runs: Laplace 1024^2 x 100 (BASELINE C1) in one launch; the fp32 wave
+    (three rotating arrays) is not a ping-pong chain and stays node by node."""
+    if mode != "resident":
+        pytest.skip("2-D chains are resident-only")
+    from oracle.oracle import laplace_reference
+    from paper_2512_19851_b200.programs import laplace_program, wave2d_program
+    prog = DagProgram()
+    names = laplace_program(prog, 1024, 100)
+    job, stats = run_program(prog, fused=True)
+    try:
+        assert _ran(job, mode)
+        assert bits_equal(job.fetch(names["u"]), laplace_reference(1024, 100))
+    finally:
+        job.close()
+    prog = DagProgram()
+    names = wave2d_program(prog, 128, 12, dtype=DTYPE_F32)
+    want = reference_execute_dag(prog.dag, prog.shapes, prog.dtypes)
+    job, _ = run_program(prog)
+    try:
+        assert not _ran(job, mode)
+        assert bits_equal(job.fetch(names["u"]), want[names["u"]])
     finally:
         job.close()

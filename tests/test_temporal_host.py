@@ -15,7 +15,7 @@ from paper_2512_19851_b200.tiles import ArrayInfo, GpuTileStore, decompose
 from paper_2512_19851_b200.wire import DTYPE_F32, DTYPE_F64
 
 
-def _executor(shapes, workers=1, odf=1, temporal_on=True):
+def _executor(shapes, workers=1, odf=1, temporal_on=True, resident_on=False):
     dev = FakeDevice()
     shape = next(iter(shapes.values()))
     decomp = decompose(shape, workers, odf)
@@ -26,6 +26,7 @@ def _executor(shapes, workers=1, odf=1, temporal_on=True):
     mgr = GpuExchangeManager(store, 0, decomp.owner_map(workers))
     ex = GpuExecutor(store, mgr)
     ex.temporal = temporal_on
+    ex.resident = resident_on
     return ex, store, mgr, dev
 
 
@@ -149,3 +150,63 @@ def test_z_star_required():
     prog.assign(b, box, heat3d_tree(a))
     plan = compile_plan(prog.dag.nodes[-1], prog.dag.ast_table)
     assert temporal.eligible(codegen.stmt_sig(plan.statements[0], 3), DTYPE_F64)
+
+
+# ---------------------------------------------------------------------------
+# resident chains (resident.py): whole L2-resident runs in one launch
+
+@pytest.mark.parametrize("iters", [2, 3, 7, 100])
+def test_resident_run_is_one_launch(iters):
+    setup, step = _heat(iters)
+    ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=True)
+    ex.execute_batch(setup.dag)
+    dev.log.clear()
+    stats = ex.execute_batch(step.dag)
+    names = _names(dev)
+    assert names == ["est_resident"]
+    assert stats.kernel_launches == iters and stats.nodes_executed == iters
+
+
+def test_resident_bookkeeping_matches_node_by_node():
+    from paper_2512_19851_b200.programs import laplace_iteration_statements, laplace_program
+    setup, step = DagProgram(), DagProgram()
+    names = laplace_program(setup, 64, 0)
+    for a in sorted(setup.shapes):
+        step.builder.declare_array(a, setup.shapes[a])
+    laplace_iteration_statements(step, names["u"], names["scratch"], 9)
+    res = []
+    for on in (True, False):
+        ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=on)
+        ex.execute_batch(setup.dag)
+        st = [ex.execute_batch(step.dag, b"k") for _ in range(4)]
+        res.append(({a: (store.local_epoch(a), store.ghost_epoch(a)) for a in store.arrays},
+                    dict(mgr.rounds_started),
+                    [(s.nodes_executed, s.kernel_launches, s.rounds, s.net_messages) for s in st]))
+    assert res[0] == res[1]
+
+
+def test_resident_needs_l2_fit_and_single_tile(monkeypatch):
+    from paper_2512_19851_b200 import resident
+    setup, step = _heat(6, n=16)
+    plans = [compile_plan(n, step.dag.ast_table) for n in step.dag.nodes]
+    ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=True)
+    assert ex.temporal_schedule(step.dag, plans)[step.dag.nodes[0].node_id] == ("res", 6)
+    monkeypatch.setattr(resident, "L2_BUDGET", 1024)
+    ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=True)
+    assert ex.temporal_schedule(step.dag, plans) == {}
+    monkeypatch.undo()
+    ex, store, mgr, dev = _executor(setup.shapes, 1, 2, temporal_on=False, resident_on=True)
+    assert ex.temporal_schedule(step.dag, plans) == {}
+
+
+def test_resident_kernel_source():
+    from paper_2512_19851_b200 import resident
+    from paper_2512_19851_b200.programs import laplace_program
+    prog = DagProgram()
+    laplace_program(prog, 32, 1)
+    plan = compile_plan(prog.dag.nodes[-1], prog.dag.ast_table)
+    sig = codegen.stmt_sig(plan.statements[0], 2)
+    assert resident.eligible(sig, DTYPE_F64, 2)
+    src, name, block, smem, geo = resident.source(sig, DTYPE_F64, 2)
+    assert name == "est_resident" and "ld.acquire.gpu" in src and "__ldcg" in src and "__stcg" in src
+    assert "__dadd_rn" in src and smem <= 48 * 1024
