@@ -34,7 +34,7 @@ from .errors import StencilError
 from .tiles import Decomposition
 from .wire import (
     INIT, PEER_HELLO, REGISTER, REPLY_ERR, REPLY_OK, W_BATCH, W_CHECKPOINT, W_CREATE, W_EXIT,
-    W_FETCH, W_MIGRATE, W_RESTORE, decode_dag, parse_json, recv_frame, send_json)
+    W_FETCH, W_MIGRATE, W_RESTORE, parse_json, recv_frame, send_json)
 
 log = logging.getLogger("elastencil.gpu_worker")
 
@@ -179,8 +179,9 @@ class GpuWorker:
         send_json(self.coord, REPLY_OK, {})
 
     def _handle_batch(self, meta: dict, blob: bytes) -> None:
-        dag = decode_dag(blob)
-        stats = self.job.run(dag)[0] if self.job is not None else None
+        # DAG-bytes cache: a repeated batch skips decode / analysis / codegen
+        # (and replays a CUDA graph on a single worker) - SURVEY.md §8f row 1
+        stats = self.job.run_bytes(blob)[0] if self.job is not None else None
         rec = {
             "batch": meta["batch"],
             "nodes": stats.nodes_executed if stats else 0,
