@@ -55,6 +55,10 @@ class TbCfg:
     l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
     persistent: bool = False
     minb: int = 0           # __launch_bounds__ min blocks per SM (0: from smem/threads, >= 48 regs)
+    variant: str = "block"  # "block" (smem ring per step) or "warp" (intermediate sweep in registers + shuffles)
+    wx: int = 2             # (warp) warps across x; each warp owns 30 output columns
+    wy: int = 4             # (warp) warps across y
+    r: int = 4              # (warp) output rows per warp
 
 
 def _env_cfg() -> TbCfg:
@@ -63,7 +67,9 @@ def _env_cfg() -> TbCfg:
     return TbCfg(k=int(e("EST_TB_K", d.k)), bx=int(e("EST_TB_BX", d.bx)), by=int(e("EST_TB_BY", d.by)),
                  rpt=int(e("EST_TB_RPT", d.rpt)), prefetch=int(e("EST_TB_PREFETCH", d.prefetch)),
                  zchunk=int(e("EST_TB_ZCHUNK", d.zchunk)), l2promo=int(e("EST_TB_L2PROMO", d.l2promo)),
-                 persistent=e("EST_TB_PERSISTENT", "0") == "1", minb=int(e("EST_TB_MINB", d.minb)))
+                 persistent=e("EST_TB_PERSISTENT", "0") == "1", minb=int(e("EST_TB_MINB", d.minb)),
+                 variant=e("EST_TB_VARIANT", d.variant), wx=int(e("EST_TB_WX", d.wx)),
+                 wy=int(e("EST_TB_WY", d.wy)), r=int(e("EST_TB_R", d.r)))
 
 
 DEFAULT = _env_cfg()
@@ -108,9 +114,19 @@ def layout(rad, dtype: int, cfg: TbCfg) -> dict:
             "cfg": cfg, "elem": elem, "q": q}
 
 
+def warp_eligible(st: StmtSig, dtype: int, cfg: TbCfg) -> bool:
+    """Warp-tiled variant: K = 2, one input slot, every offset within +-1, z-star."""
+    if cfg.variant != "warp" or cfg.k != 2 or st.arity != 1 or dtype not in ELEM or not z_star(st):
+        return False
+    rad = slot_radius(st).get(0)
+    return rad is not None and max(rad) <= 1 and rad[0] == 1 and cfg.r >= 1
+
+
 def eligible(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> bool:
     """Single input slot, z-star loads, 1 <= rz, radius <= MAX_RADIUS, fits."""
     cfg = cfg or DEFAULT
+    if warp_eligible(st, dtype, cfg):
+        return True
     if cfg.k < 2 or cfg.k % 2 or st.arity != 1 or dtype not in ELEM or not z_star(st):
         return False
     rad = slot_radius(st).get(0)
@@ -127,6 +143,13 @@ def blocks_per_sm(smem: int, nt: int) -> int:
 
 
 def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
+    cfg = cfg or DEFAULT
+    if warp_eligible(st, dtype, cfg):
+        return source_warp(st, dtype, cfg)
+    return source_block(st, dtype, cfg)
+
+
+def source_block(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
     """-> (source, kernel name, block, smem, geometry).
 
     Each compute thread owns RPT points of the step-1 region (W1 x H1, rows
@@ -276,6 +299,196 @@ def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
     src = "\n".join(L) + "\n"
     lay["blocks_per_sm"] = minb
     return src, "est_tb", (NT + 32, 1, 1), lay["smem"], lay
+
+
+def source_warp(st: StmtSig, dtype: int, cfg: TbCfg) -> tuple:
+    """K = 2 warp-tiled chain kernel.
+
+    CTA output tile = (30*WX) x (R*WY) columns x rows, streamed along z; the
+    producer warp TMA-loads each input plane (tile + 2-cell halo) into an
+    mbarrier ring. Each compute warp owns 30 output columns x R rows: lane l
+    holds column l-1, so lanes 0 and 31 carry the x-halo of the intermediate
+    sweep. Step 1 (B at t+1) is computed for rows -1..R of the warp from the
+    shared input plane (z-neighbours from a per-lane register window); step 2
+    (A at t+2) reads step 1 only from registers: own rows / y-neighbours
+    directly, x-neighbours through warp shuffles. No shared memory for the
+    intermediate sweep and no barrier between warps."""
+    rz, ry, rx = slot_radius(st)[0]
+    T = CTYPE[dtype]
+    elem = ELEM[dtype]
+    q = 16 // elem
+    WX, WY, R = cfg.wx, cfg.wy, cfg.r
+    BX, BY = 30 * WX, R * WY
+    NW = WX * WY
+    NT = 32 * NW
+    w0 = _round(BX + 4 + q - 1, q)
+    h0 = BY + 4
+    s0 = 2 + cfg.prefetch
+    pl0 = _round(w0 * h0 * elem, 1024)
+    data = s0 * pl0
+    smem = data + 8 * 2 * s0 + 1024
+    minb = cfg.minb or max(1, min(SMEM_PER_SM // (smem + 1024), 65536 // ((NT + 32) * 96), 2048 // (NT + 32)))
+    lay = {"rad": (rz, ry, rx), "w0": w0, "h0": h0, "s0": s0, "pl0": pl0, "data": data, "smem": smem,
+           "cfg": cfg, "elem": elem, "q": q, "bx": BX, "by": BY, "nt": NT, "min_blocks": minb,
+           "blocks_per_sm": minb, "variant": "warp"}
+    ROWS = list(range(-1, R + 1))          # step-1 rows of a warp (rr = r + 1)
+    L = []
+    a = L.append
+    a(f'// generated by paper_2512_19851_b200/temporal.py — skeleton "tb" warp-tiled (K=2) {cfg}')
+    a(f"typedef {T} T;")
+    a("struct __align__(64) Tmap { unsigned long long w[16]; };")
+    a("struct __align__(64) Params { Tmap tm;")
+    a("  unsigned long long src, bhome, adst;  // padded-box origins: A now, B (in place), A next")
+    a("  long long py, pz;")
+    a("  int npz, npy, npx, xoff, sz0, sz1, sy0, sy1, sx0, sx1, nbx, nby, zc, nzc; };")
+    L.append(_PTX_HELPERS)
+    a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
+    a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
+    a(f'extern "C" __global__ void __launch_bounds__({NT + 32}, {minb})')
+    a("est_tb(const __grid_constant__ Params p) {")
+    a("  extern __shared__ __align__(1024) unsigned char smem[];")
+    a(f"  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + {data});")
+    a(f"  unsigned long long* empty = full + {s0};")
+    a("  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;")
+    a("  const int n_items = p.nbx * p.nby * p.nzc;")
+    a("  if (tid == 0) {")
+    a(f"    for (int i = 0; i < {s0}; ++i) {{ mbar_init(full + i, 1); mbar_init(empty + i, {NW}); }}")
+    a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
+    a("  }")
+    a("  __syncthreads();")
+
+    def item_decode(ind):
+        a(f"{ind}const int bx = item % p.nbx, rest = item / p.nbx;")
+        a(f"{ind}const int by = rest % p.nby, bzc = rest / p.nby;")
+        a(f"{ind}const int x0 = p.sx0 + bx * {BX}, y0 = p.sy0 + by * {BY};")
+        a(f"{ind}const int zs = p.sz0 + bzc * p.zc;")
+        a(f"{ind}const int nzl = min(p.zc, p.sz1 - zs);")
+        a(f"{ind}const int n0 = nzl + 4;")
+
+    # ---------------- producer warp
+    a(f"  if (warp == {NW}) {{")
+    a("    if (lane != 0) return;")
+    a("    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm) : \"memory\");")
+    a("    int fill = 0;")
+    a("    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+    item_decode("      ")
+    a("      const int xs = p.xoff + x0 - 2;")
+    a(f"      const int xa = xs - (xs & {q - 1});")
+    a("      for (int k = 0; k < n0; ++k) {")
+    a(f"        const int g = fill + k, stg = g % {s0};")
+    a(f"        if (g >= {s0}) mbar_wait(empty + stg, ((g / {s0}) - 1) & 1);")
+    a(f"        mbar_expect(full + stg, {w0 * h0 * elem});")
+    a(f"        tma_load3(smem + stg * {pl0}, &p.tm, xa, y0 - 2, zs - 2 + k, full + stg);")
+    a("      }")
+    a("      fill += n0;")
+    a("    }")
+    a("    return;")
+    a("  }")
+    # ---------------- compute warps
+    a("  const T* __restrict__ asrc = reinterpret_cast<const T*>(p.src); (void)asrc;")
+    a("  T* __restrict__ bmem = reinterpret_cast<T*>(p.bhome);")
+    a("  T* __restrict__ adst = reinterpret_cast<T*>(p.adst);")
+    a(f"  const int wxi = warp % {WX}, wyi = warp / {WX};")
+    a("  const bool own = lane >= 1 && lane <= 30;")
+    a("  const long long py = p.py, pz = p.pz;")
+    a("  int fill = 0;")
+    for j in (0, 1):
+        for rr in range(len(ROWS)):
+            a(f"  T {', '.join(f'c{j}_{rr}_{k} = 0' for k in range(3))};")
+    a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+    item_decode("    ")
+    a(f"    const int sh = (p.xoff + x0 - 2) & {q - 1};")
+    a(f"    const int scol = sh + 30 * wxi + lane + 1;   // smem column of this lane (output column lane-1)")
+    a(f"    const int srow = {R} * wyi + 2;               // smem row of warp row 0")
+    a("    const int gx = x0 + 30 * wxi + lane - 1;")
+    a("    const bool colS = gx >= p.sx0 && gx < p.sx1, colP = gx >= 0 && gx < p.npx;")
+    a(f"    const int gy0 = y0 + {R} * wyi;")
+    for rr, r in enumerate(ROWS):
+        a(f"    const bool rS{rr} = (gy0 + {r}) >= p.sy0 && (gy0 + {r}) < p.sy1 && colS;")
+        a(f"    const bool rP{rr} = (gy0 + {r}) >= 0 && (gy0 + {r}) < p.npy && colP;")
+    a("    const long long cb = (long long)gy0 * py + gx;  // row-0 offset of this lane within a plane")
+    a("    const T* ring = reinterpret_cast<const T*>(smem) + sh * 0;")
+    a(f"    for (int t0 = 0; t0 < n0; t0 += 3) {{")
+    for m in range(3):
+        def col(j, rr, k, m=m):
+            return f"c{j}_{rr}_{(k + m) % 3}"
+        a(f"      if (t0 + {m} < n0) {{")
+        a(f"      const int t = t0 + {m};")
+        a(f"      {{ const int g = fill + t; mbar_wait(full + g % {s0}, (g / {s0}) & 1); }}")
+        a(f"      const T* Pn = ring + ((fill + t) % {s0}) * {pl0 // elem} + srow * {w0} + scol;  // input plane t")
+        for rr, r in enumerate(ROWS):
+            a(f"      {col(0, rr, 2)} = Pn[{r * w0}];")
+        # ---- step 1: plane index t-1 of the input is the centre plane
+        a("      if (t >= 2) {")
+        a(f"        const T* Pc = ring + ((fill + t - 1) % {s0}) * {pl0 // elem} + srow * {w0} + scol;")
+        a("        const int z1 = zs - 1 + (t - 2);")
+        a("        const bool zin1 = z1 >= p.sz0 && z1 < p.sz1, zp1 = z1 >= 0 && z1 < p.npz;")
+        a("        const long long zo1 = (long long)z1 * pz + cb;")
+        for rr, r in enumerate(ROWS):
+            def load1(slot, off3, rr=rr, r=r):
+                dz, dy, dx = off3
+                if dz != 0 or (dy == 0 and dx == 0):
+                    return col(0, rr, 1 + dz)
+                if dx == 0 and 0 <= rr + dy < len(ROWS):
+                    return col(0, rr + dy, 1)
+                return f"Pc[{(r + dy) * w0 + dx}]"
+            lines, res = _emit_expr(st, dtype, load1)
+            a(f"        {{ T v;")
+            a(f"          if (zin1 && rS{rr}) {{")
+            for ln in lines:
+                a(f"            {ln}")
+            a(f"            v = {res};")
+            if 0 <= r < R:
+                a(f"            if (own) bmem[zo1 + {r} * py] = v;")
+            a(f"          }} else {{")
+            a(f"            v = (zp1 && rP{rr}) ? bmem[zo1 + {r} * py] : ({T})0;  // outside S: stored value")
+            a("          }")
+            a(f"          {col(1, rr, 2)} = v; }}")
+        a("      }")
+        a(f"      if (t >= 1) {{ __syncwarp(); if (lane == 0) mbar_arrive(empty + (fill + t - 1) % {s0}); }}")
+        # ---- step 2: step-1 index t-3 is the centre
+        a("      if (t >= 4) {")
+        a("        const int z2 = zs + (t - 4);")
+        a("        const bool zin2 = z2 >= p.sz0 && z2 < p.sz1;")
+        a("        const long long zo2 = (long long)z2 * pz + cb;")
+        # shuffled neighbours needed
+        need = set()
+        for i in st.instructions:
+            if i[0] == "load" and i[2][0] == 0 and i[2][2] != 0:
+                need.add((i[2][1], i[2][2]))
+        shf = {}
+        for r in range(R):
+            rr = r + 1
+            for dy, dx in sorted(need):
+                key = (rr + dy, dx)
+                if key not in shf:
+                    nm = f"sf{rr + dy}_{'m' if dx < 0 else 'p'}{abs(dx)}"
+                    shf[key] = nm
+                    a(f"        const T {nm} = __shfl_sync(0xffffffffu, {col(1, rr + dy, 1)}, (lane + ({dx})) & 31);")
+        for r in range(R):
+            rr = r + 1
+            def load2(slot, off3, rr=rr):
+                dz, dy, dx = off3
+                if dz != 0 or (dy == 0 and dx == 0):
+                    return col(1, rr, 1 + dz)
+                if dx == 0:
+                    return col(1, rr + dy, 1)
+                return shf[(rr + dy, dx)]
+            lines, res = _emit_expr(st, dtype, load2)
+            a(f"        if (zin2 && rS{rr} && own) {{")
+            for ln in lines:
+                a(f"          {ln}")
+            a(f"          adst[zo2 + {r} * py] = {res};")
+            a("        }")
+        a("      }")
+        a("      }")
+    a("    }")
+    a(f"    if (lane == 0) mbar_arrive(empty + (fill + n0 - 1) % {s0});")
+    a("    fill += n0;")
+    a("  }")
+    a("}")
+    src = "\n".join(L) + "\n"
+    return src, "est_tb", (NT + 32, 1, 1), smem, lay
 
 
 def emit_fast_loop(a, st: StmtSig, dtype: int, lay: dict) -> None:
@@ -443,7 +656,7 @@ def item_geometry(s_lo, s_hi, sm_count: int, lay: dict) -> dict:
     """Work-item tiling of the output box S (padded coordinates)."""
     cfg = lay["cfg"]
     nz, ny, nx = (b - a for a, b in zip(s_lo, s_hi))
-    nbx, nby = -(-nx // cfg.bx), -(-ny // cfg.by)
+    nbx, nby = -(-nx // lay.get("bx", cfg.bx)), -(-ny // lay.get("by", cfg.by))
     zc = min(cfg.zchunk, nz)
     nzc = -(-nz // zc)
     n_items = nbx * nby * nzc
