@@ -21,12 +21,16 @@ from paper_2512_19851_b200.wire import DTYPE_F32, encode_dag
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["tb", "resident"])
+@pytest.fixture(autouse=True, params=["tb", "tb-warp", "resident"])
 def mode(request, monkeypatch):
+    import dataclasses
+
     from paper_2512_19851_b200 import resident, temporal
-    monkeypatch.setattr(temporal, "ENABLED", request.param == "tb")
+    monkeypatch.setattr(temporal, "ENABLED", request.param.startswith("tb"))
     monkeypatch.setattr(resident, "ENABLED", request.param == "resident")
-    return request.param
+    if request.param == "tb-warp":
+        monkeypatch.setattr(temporal, "DEFAULT", dataclasses.replace(temporal.DEFAULT, variant="warp"))
+    return "tb" if request.param.startswith("tb") else request.param
 
 
 def _ran(job, mode) -> bool:
