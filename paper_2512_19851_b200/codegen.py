@@ -261,8 +261,11 @@ def kernel_source_for(plan, rank: int, dtype: int, skeleton: str = "auto", small
         return hit
     stmts = tuple(stmt_sig(p, rank) for p in plan.statements)
     skel = "point"
-    if skeleton in ("auto", "stream") and stream_eligible(stmts, rank, dtype, cfg):
-        skel = "stream"
+    if skeleton in ("auto", "stream"):
+        for c in stream.fallback_cfgs(rank, small):
+            if stream_eligible(stmts, rank, dtype, c):
+                skel, cfg = "stream", c
+                break
     sig = NodeSig(dtype, stmts, skel)
     res = (*(stream_source(sig, rank, cfg) if skel == "stream" else point_source(sig, rank)), sig)
     _SRC_CACHE[key] = res

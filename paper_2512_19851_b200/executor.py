@@ -27,7 +27,7 @@ import time
 from dataclasses import dataclass, field
 
 from . import codegen, resident, stream, temporal
-from .analysis import analyze_dag, compile_plan
+from .analysis import KernelPlan, analyze_dag, compile_plan
 from .device import COMPUTE
 from .errors import MalformedDag
 
@@ -590,12 +590,45 @@ class GpuExecutor:
             return False
         return codegen.kernel_source_for(plan, 3, info.dtype, self.skeleton)[6].skeleton == "stream"
 
+    SPLIT_MIN_POINTS = 1 << 16
+
+    def _split_fused(self, plan, boxes, rank: int, dtype: int):
+        """A fused node's statements are independent (ir.fuse, executor.py:320-324
+        order is irrelevant then): large statements the stream skeleton can
+        take get their own stream launch, the rest share one point launch.
+        Returns the sub-plans, or None to keep the node whole."""
+        if len(plan.statements) < 2 or self.skeleton not in ("auto", "stream"):
+            return None
+        pts: dict = {}
+        for si, _ps, _tile, _lo, n in boxes:
+            k = 1
+            for e in n:
+                k *= e
+            pts[si] = pts.get(si, 0) + k
+        big, rest = [], []
+        for si, ps in enumerate(plan.statements):
+            sub = KernelPlan(plan.node_id, (ps,))
+            if (pts.get(si, 0) >= self.SPLIT_MIN_POINTS and codegen.kernel_source_for(
+                    sub, rank, dtype, self.skeleton, rank == 2 and pts[si] < stream.SMALL_2D_POINTS)[6].skeleton == "stream"):
+                big.append(sub)
+            else:
+                rest.append(ps)
+        if not big:
+            return None
+        return big + ([KernelPlan(plan.node_id, tuple(rest))] if rest else [])
+
     def _launch_node(self, node, plan, zsplit=None) -> None:
         boxes = self._boxes(plan)
         if not boxes:
             return
         info = self.store.arrays[plan.statements[0].output]
         rank, dtype = info.rank, info.dtype
+        if zsplit is None:
+            parts = self._split_fused(plan, boxes, rank, dtype)
+            if parts is not None:
+                for sub in parts:
+                    self._launch_node(node, sub, None)
+                return
         small = rank == 2 and sum(n[0] * n[1] for *_x, n in boxes) < stream.SMALL_2D_POINTS
         src, name, block, smem, n_items, geom, sig = codegen.kernel_source_for(
             plan, rank, dtype, self.skeleton, small)

@@ -103,6 +103,20 @@ DEFAULT_2D_SMALL = StreamCfg(bx=128, by=16, ty=4, prefetch=3, persistent=True, w
                              l2promo=2, v2=True)
 
 
+def fallback_cfgs(rank: int, small: bool = False) -> list:
+    """Configurations to try in order: the default, then shorter tiles, so
+    multi-input statements whose rings do not fit the default tile's shared
+    memory (e.g. cavity flow's 3-input momentum updates) still stream."""
+    first = cfg_for(rank, small)
+    out = [first]
+    for by in (16, 8, 4):
+        if by < first.by:
+            out.append(StreamCfg(bx=first.bx, by=by, ty=min(first.ty, by), prefetch=min(first.prefetch, 2),
+                                 persistent=first.persistent, zchunk=first.zchunk, l2promo=first.l2promo,
+                                 ws=True, zreg=first.zreg, v2=first.v2))
+    return out
+
+
 def cfg_for(rank: int, small: bool = False) -> StreamCfg:
     """Rank-3 nodes stream along z; rank-2 nodes run the same warp-specialised
     TMA pipeline on a (1, Y, X) view: every item is one (BY+2ry) x (BX+2rx)

@@ -248,3 +248,20 @@ def test_large_2d_tiles_bit_exact():
         assert bits_equal(job.fetch(names["u"]), laplace_reference(3000, 5))
     finally:
         job.close()
+
+
+def test_fused_cavity_split_into_stream_launches():
+    """Fused nodes whose independent statements are large run one stream launch
+    per statement (plus one point launch for the small rest); bit-exact."""
+    from paper_2512_19851_b200.programs import cavity_program
+    prog = DagProgram()
+    names = cavity_program(prog, 512, 2)
+    want = reference_execute_dag(prog.dag, prog.shapes)
+    job, stats = run_program(prog, fused=True)
+    try:
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), aid
+        # kernel_launches keeps the reference definition (one per node per tile)
+        assert sum(s.kernel_launches for b in stats for s in b) == sum(s.nodes_executed for b in stats for s in b)
+    finally:
+        job.close()
