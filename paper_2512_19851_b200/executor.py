@@ -26,7 +26,7 @@ from __future__ import annotations
 import time
 from dataclasses import dataclass, field
 
-from . import codegen, resident, stream, temporal
+from . import codegen, resident, stream, temporal, wavefront
 from .analysis import KernelPlan, analyze_dag, compile_plan
 from .device import COMPUTE
 from .errors import MalformedDag
@@ -85,6 +85,8 @@ class GpuExecutor:
         self.replays = 0
         self.temporal = temporal.ENABLED  # fuse ping-pong sweep chains (temporal.py)
         self.resident = resident.ENABLED  # whole L2-resident chains in one launch (resident.py)
+        self.wave = wavefront.ENABLED     # sweep pairs forwarded through L2 in one launch (wavefront.py)
+        self._wave_ctr = (0, 0)           # (device pointer, bytes) of the wave ticket/progress counters
         self._bar = 0                     # grid-barrier counter of the resident skeleton
         self.tb_cfg = temporal.DEFAULT
         self._scratch: dict = {}     # array -> twin TileBuffer for temporal chains
@@ -247,6 +249,9 @@ class GpuExecutor:
         if self._bar:
             self.dev.free(self._bar)
             self._bar = 0
+        if self._wave_ctr[0]:
+            self.dev.free(self._wave_ctr[0])
+            self._wave_ctr = (0, 0)
 
     # -- execution (executor.py:258-348) ------------------------------------
     def _execute(self, dag, key: bytes | None = None) -> BatchStats:
@@ -281,6 +286,8 @@ class GpuExecutor:
                     self._launch_tb(node, plan, chain[1], key)
                 elif chain[0] == "res":
                     self._launch_resident(node, plan, chain[1], key)
+                elif chain[0] == "wave":
+                    self._launch_wave(node, plan, key)
             elif pending and set(pending) & set(meta.array_max_offset) and self.overlap_eligible(plan):
                 # halo/compute overlap: planes that read no ghost cells go first,
                 # the deferred peer pull runs on the copy lane meanwhile, the
@@ -350,11 +357,12 @@ class GpuExecutor:
         the number of chains kept even so A ends in its own buffer. Only for
         one tile per job without transport (no exchange between sweeps);
         everything else runs node by node."""
-        if (not (self.temporal or self.resident) or self.transport is not None
+        if (not (self.temporal or self.resident or self.wave) or self.transport is not None
                 or len(self.store.tiles) != 1 or self.store.decomp.n_tiles != 1
                 or self.skeleton not in ("auto", "tb")):
             return {}
-        ck = (key, self.store.version, self.tb_cfg, self.temporal, self.resident) if key is not None else None
+        ck = ((key, self.store.version, self.tb_cfg, self.temporal, self.resident, self.wave)
+              if key is not None else None)
         hit = self._tb_sched.get(ck) if ck is not None else None
         if hit is not None:
             return hit
@@ -378,6 +386,10 @@ class GpuExecutor:
                 sched[dag.nodes[i].node_id] = ("res", j - i)
                 for q in range(i + 1, j):
                     sched[dag.nodes[q].node_id] = ("member",)
+            elif self.wave and c[4] == 3 and wavefront.eligible(sig, c[5]):
+                for ch in range((j - i) // 2):
+                    sched[dag.nodes[i + 2 * ch].node_id] = ("wave", ch)
+                    sched[dag.nodes[i + 2 * ch + 1].node_id] = ("member",)
             elif self.temporal and c[4] == 3 and temporal.eligible(sig, c[5], self.tb_cfg):
                 m = (j - i) // K
                 m -= m % 2
@@ -392,6 +404,51 @@ class GpuExecutor:
                 self._tb_sched.clear()
             self._tb_sched[ck] = sched
         return sched
+
+    def _launch_wave(self, node, plan, key) -> None:
+        """Two sweeps (this node and the next) in one launch, in place (wavefront.py)."""
+        ps = plan.statements[0]
+        a, b = ps.inputs[0], ps.output
+        tile = next(iter(self.store.tiles.values()))
+        ba, bb = tile.buffers[a], tile.buffers[b]
+        info = self.store.arrays[a]
+        cfg = wavefront.DEFAULT
+        d = ba.depth
+        s_lo = tuple(lo + dd for (lo, _), dd in zip(ps.output_slice_bounds, d))
+        s_hi = tuple(hi + dd for (_, hi), dd in zip(ps.output_slice_bounds, d))
+        geo = wavefront.geometry(s_lo, s_hi, cfg)
+        need = 4 * (1 + geo["nzb"])
+        ptr, size = self._wave_ctr
+        if size < need:
+            if ptr:
+                self.dev.free(ptr)
+            size = max(need, 4096)
+            ptr = self.dev.alloc(size)
+            self._wave_ctr = (ptr, size)
+        self.dev.memset_zero(ptr, need, COMPUTE)
+        ck = (key, node.node_id, self.store.version, "wave") if key is not None else None
+        rec = self._launches.get(ck) if ck is not None else None
+        if rec is not None and not self.time_kernels:
+            for kern, grid, params in rec:
+                self.dev.launch(kern, grid, params, COMPUTE)
+            return
+        sig = codegen.stmt_sig(ps, 3)
+        src, name, block, smem, wgeo = wavefront.source(sig, info.dtype, cfg)
+        kern = self.dev.kernel(src, name, block, smem)
+        tmA = self._tmap(ba, wgeo["box"], cfg.l2promo)
+        tmB = self._tmap(bb, wgeo["box"], cfg.l2promo)
+        params = wavefront.pack_params(tmA, tmB, ba.addr(*s_lo), bb.addr(*s_lo), ptr, ba.py, ba.pz,
+                                       ba.xoff + s_lo[2], s_lo[1], s_lo[0], geo)
+        occ = self.dev.occupancy(kern)
+        if occ < 1:
+            raise RuntimeError("wave kernel cannot be resident on this device")
+        self._recording = [] if ck is not None else None
+        try:
+            self._launch(kern, (self.dev.sm_count, 1, 1), params, tag=("tb", 2))
+        finally:
+            rec, self._recording = self._recording, None
+        if ck is not None and rec is not None:
+            self._launches[ck] = rec
 
     def _launch_resident(self, node, plan, sweeps: int, key) -> None:
         """One persistent launch running `sweeps` ping-pong sweeps in L2."""

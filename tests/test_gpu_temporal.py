@@ -21,13 +21,14 @@ from paper_2512_19851_b200.wire import DTYPE_F32, encode_dag
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["tb", "tb-warp", "resident"])
+@pytest.fixture(autouse=True, params=["tb", "tb-warp", "resident", "wave"])
 def mode(request, monkeypatch):
     import dataclasses
 
-    from paper_2512_19851_b200 import resident, temporal
+    from paper_2512_19851_b200 import resident, temporal, wavefront
     monkeypatch.setattr(temporal, "ENABLED", request.param.startswith("tb"))
     monkeypatch.setattr(resident, "ENABLED", request.param == "resident")
+    monkeypatch.setattr(wavefront, "ENABLED", request.param == "wave")
     if request.param == "tb-warp":
         monkeypatch.setattr(temporal, "DEFAULT", dataclasses.replace(temporal.DEFAULT, variant="warp"))
     return "tb" if request.param.startswith("tb") else request.param
@@ -35,7 +36,7 @@ def mode(request, monkeypatch):
 
 def _ran(job, mode) -> bool:
     ex = job.executors[0]
-    return bool(ex._scratch) if mode == "tb" else bool(ex._bar)
+    return {"tb": bool(ex._scratch), "resident": bool(ex._bar), "wave": bool(ex._wave_ctr[0])}[mode]
 
 
 def _tb_launches(stats) -> int:
@@ -160,7 +161,7 @@ def test_repeated_batches_graph_replay_bit_exact(mode):
         assert job.executors[0].replays >= 2
         # tb: 10 sweeps = 4 chains of 2 (chain count kept even) + 2 single sweeps
         # + the complement copy; resident: the whole batch is one launch
-        assert stats[1][0].gpu_launches == (4 + 2 + 1 if mode == "tb" else 1)
+        assert stats[1][0].gpu_launches == {"tb": 4 + 2 + 1, "resident": 1, "wave": 5}[mode]
         for aid in setup.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), aid
 
@@ -177,6 +178,7 @@ def test_chain_disabled_equals_enabled(mode):
                 job.create_array(prog.shapes[aid])
             job.executors[0].temporal = on and mode == "tb"
             job.executors[0].resident = on and mode == "resident"
+            job.executors[0].wave = on and mode == "wave"
             job_stats = job.run(prog.dag)
             outs.append([job.fetch(a) for a in sorted(prog.shapes)])
             assert _ran(job, mode) == on
@@ -203,7 +205,7 @@ def test_non_z_star_chain(mode):
     want = reference_execute_dag(prog.dag, prog.shapes)
     job, _ = run_program(prog)
     try:
-        assert _ran(job, mode) == (mode == "resident")
+        assert _ran(job, mode) == (mode in ("resident", "wave"))
         for aid in prog.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), aid
     finally:

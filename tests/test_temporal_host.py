@@ -27,6 +27,7 @@ def _executor(shapes, workers=1, odf=1, temporal_on=True, resident_on=False):
     ex = GpuExecutor(store, mgr)
     ex.temporal = temporal_on
     ex.resident = resident_on
+    ex.wave = False
     return ex, store, mgr, dev
 
 
@@ -210,3 +211,46 @@ def test_resident_kernel_source():
     src, name, block, smem, geo = resident.source(sig, DTYPE_F64, 2)
     assert name == "est_resident" and "ld.acquire.gpu" in src and "__ldcg" in src and "__stcg" in src
     assert "__dadd_rn" in src and smem <= 48 * 1024
+
+
+@pytest.mark.parametrize("iters", [2, 5, 8])
+def test_wave_pairs(iters):
+    setup, step = _heat(iters)
+    ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=False)
+    ex.wave = True
+    ex.execute_batch(setup.dag)
+    dev.log.clear()
+    stats = ex.execute_batch(step.dag)
+    names = _names(dev)
+    assert names.count("est_wave") == iters // 2
+    assert names.count("est_stream") == iters % 2
+    assert stats.kernel_launches == iters
+
+
+def test_wave_kernel_source():
+    from paper_2512_19851_b200 import wavefront
+    prog = DagProgram()
+    heat3d_setup(prog, 32)
+    prog.assign(1, (slice(1, -1),) * 3, heat3d_tree(0))
+    plan = compile_plan(prog.dag.nodes[-1], prog.dag.ast_table)
+    sig = codegen.stmt_sig(plan.statements[0], 3)
+    assert wavefront.eligible(sig, DTYPE_F64)
+    src, name, block, smem, geo = wavefront.source(sig, DTYPE_F64)
+    assert name == "est_wave" and "fence.proxy.async.global" in src and "ld.acquire.gpu" in src
+    assert "atomicAdd(ctr, 1u)" in src and smem <= 227 * 1024
+
+
+@pytest.mark.parametrize("nxy,nzb", [(1, 1), (3, 1), (4, 2), (5, 3), (64, 16), (2, 7)])
+def test_wave_ticket_order_is_deadlock_free(nxy, nzb):
+    """Every ticket is dispensed once and each sweep-2 item's dependencies
+    (all sweep-1 tiles of z-blocks b-1..b+1) hold earlier tickets."""
+    from paper_2512_19851_b200.wavefront import decode
+    n1 = nxy * nzb
+    pos = {}
+    for t in range(2 * n1):
+        pos[decode(t, nxy, n1, 2)] = t
+    assert len(pos) == 2 * n1
+    for i in range(n1):
+        zb = i // nxy
+        for b in range(max(zb - 1, 0), min(zb + 1, nzb - 1) + 1):
+            assert all(pos[(1, b * nxy + k)] < pos[(2, i)] for k in range(nxy))
