@@ -103,9 +103,10 @@ def migrate_tiles(job, plan: dict) -> dict:
     new_map = {c: new for c, (_old, new) in plan.items()}
     job.set_owner_map(new_map)
     for a in sorted(store.arrays):
+        # every worker, tile-less or not, continues from the job-wide epoch
+        store.set_epochs(a, epochs.get(a, 0), epochs.get(a, 0))
         store.bump_local_epoch(a)
-        for tile in store.tiles.values():
-            tile.ghost_epoch[a] = tile.local_epoch[a] - 1
+        store.set_ghost_epoch(a, store.local_epoch(a) - 1)
     t2 = time.perf_counter()
     job.exchange_buffers()
     return {"tiles_in": len(incoming), "tiles_out": len(outgoing), "bytes_in": nbytes,
@@ -198,6 +199,9 @@ def restore_tiles(job, manifest: dict) -> dict:
         a = int(key)
         store.arrays[a] = ArrayInfo(a, tuple(meta["shape"]), int(meta.get("dtype", 0)))
         depths[a] = tuple(meta["depth"])
+        # the job-wide epochs, so workers restored without tiles keep the round
+        # sequence aligned (tiles, if any, carry the same values in their blobs)
+        store.set_epochs(a, int(meta.get("local_epoch", 0)), int(meta.get("local_epoch", 0)))
     clients: dict = {}
     opened = []  # (client, alloc id, mapped address): all copies in flight, ONE sync
     try:

@@ -202,8 +202,7 @@ class GpuExchangeManager:
             self.copy_launches += 1
         self.rounds_started[array] = self.rounds_started.get(array, 0) + 1
         self.completed[array] = epoch
-        for tile in self.store.tiles.values():
-            tile.ghost_epoch[array] = epoch
+        self.store.set_ghost_epoch(array, epoch)
         return True
 
     def round_complete(self, array: int, epoch: int) -> bool:

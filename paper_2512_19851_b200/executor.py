@@ -224,12 +224,10 @@ class GpuExecutor:
                 continue
             dl, grel, dr = e
             start = st.local_epoch(a)
-            for tile in st.tiles.values():
-                tile.local_epoch[a] += dl
+            st.bump_local_epoch(a, dl)
             if grel is not None:
                 ex.completed[a] = start + grel
-                for tile in st.tiles.values():
-                    tile.ghost_epoch[a] = start + grel
+                st.set_ghost_epoch(a, start + grel)
             if dr:
                 ex.rounds_started[a] = ex.rounds_started.get(a, 0) + dr
         s = ent["stats"]

@@ -189,6 +189,8 @@ class GpuTileStore:
         self.tiles: dict = {c: GpuTile(c) for c in owned}
         self.arrays: dict = {}
         self.version = 0  # bumped whenever any buffer is (re)allocated or dropped
+        self._epochs: dict = {}  # array -> local epoch (also valid with no tiles)
+        self._ghosts: dict = {}
 
     # -- creation / capacity ------------------------------------------------
     def create_array(self, info: ArrayInfo) -> None:
@@ -199,6 +201,8 @@ class GpuTileStore:
         self.decomp.check_divisible(info.shape)
         self.arrays[info.array] = info
         self.version += 1
+        self._epochs[info.array] = 0
+        self._ghosts[info.array] = 0
         ext = self.decomp.tile_extents(info.shape)
         zero = (0,) * info.rank
         for tile in self.tiles.values():
@@ -239,15 +243,34 @@ class GpuTileStore:
         return NP_DTYPE[self.arrays[array].dtype]
 
     # -- epochs (grid.py:192-206) -------------------------------------------
-    def bump_local_epoch(self, array: int) -> None:
+    # Epochs are uniform over a worker's tiles; the store also keeps them per
+    # array so a worker that owns no tile (after a shrink-by-migration, or
+    # expanded past the initial owners) keeps counting with everyone else and
+    # takes part in every halo round - the transport sequences rounds globally.
+    def bump_local_epoch(self, array: int, by: int = 1) -> None:
         for tile in self.tiles.values():
-            tile.local_epoch[array] += 1
+            tile.local_epoch[array] += by
+        self._epochs[array] = self._epochs.get(array, 0) + by
+
+    def set_epochs(self, array: int, local: int, ghost: int) -> None:
+        for tile in self.tiles.values():
+            tile.local_epoch[array] = local
+            tile.ghost_epoch[array] = ghost
+        self._epochs[array] = local
+        self._ghosts[array] = ghost
+
+    def set_ghost_epoch(self, array: int, ghost: int) -> None:
+        for tile in self.tiles.values():
+            tile.ghost_epoch[array] = ghost
+        self._ghosts[array] = ghost
 
     def _uniform(self, attr: str, array: int) -> int:
         vals = {getattr(t, attr)[array] for t in self.tiles.values()}
         if len(vals) > 1:
             raise AssertionError(f"non-uniform {attr} for array {array}")
-        return vals.pop() if vals else 0
+        if vals:
+            return vals.pop()
+        return (self._epochs if attr == "local_epoch" else self._ghosts).get(array, 0)
 
     def local_epoch(self, array: int) -> int:
         return self._uniform("local_epoch", array)

@@ -76,3 +76,41 @@ def gpu_rank(rank, world, kind, odf, batch):
     rounds = job.rounds_by_array()
     job.close()
     return {"ok": ok, "rounds": rounds}
+
+
+def migrate_rank(rank, world, kind, shrink_to):
+    """CPU: fake device; run, migrate every tile onto `shrink_to` workers (the
+    rest own nothing), run, migrate back, run. Rounds must stay globally
+    sequenced (tile-less workers keep counting epochs)."""
+    import paper_2512_19851_b200.ipc as ipc
+    from fakedev import FakeDevice
+
+    ipc.Device = lambda device=0: FakeDevice(device, tag=f"r{rank}")
+    from paper_2512_19851_b200.elastic import migrate_tiles
+
+    prog, _ = _program(kind)
+    parts = _split(prog.dag, max(1, len(prog.dag.nodes) // 3))
+    job = ipc.IpcGpuJob(rank, world, timeout_s=60.0)
+    for aid in sorted(prog.shapes):
+        job.create_array(prog.shapes[aid])
+    seqs = []
+
+    def move(workers):
+        old = dict(job.owner_map)
+        new = job.decomp.owner_map(workers)
+        migrate_tiles(job, {c: (old[c], new[c]) for c in old})
+
+    job.run(parts[0])
+    seqs.append(job.transport.seq)
+    move(shrink_to)
+    tiles_shrunk = sorted(job.store.tiles)
+    for part in parts[1:-1]:
+        job.run(part)
+    seqs.append(job.transport.seq)
+    move(world)
+    job.run(parts[-1])
+    seqs.append(job.transport.seq)
+    out = {"seqs": seqs, "tiles_shrunk": tiles_shrunk,
+           "epochs": {a: job.store.local_epoch(a) for a in prog.shapes}}
+    job.close()
+    return out

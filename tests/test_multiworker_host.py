@@ -34,3 +34,17 @@ def test_rounds_and_handshake_across_processes(kind, world, odf, batch):
         assert all(r["copy_lane_pulls"] > 0 for r in res)
     tiles = sorted(t for r in res for t in r["tiles"])
     assert len(tiles) == len(set(tiles)) == world * odf
+
+
+@pytest.mark.parametrize("kind,world,shrink_to", [("heat3d", 4, 2), ("laplace", 4, 2), ("heat3d", 4, 1)])
+def test_migration_keeps_tileless_workers_in_sequence(kind, world, shrink_to):
+    """After a shrink-by-migration some workers own no tile; they still count
+    epochs and take part in every round, so after migrating back the round
+    sequence is aligned on every worker (a misalignment deadlocks the IPC
+    handshake and fails this test by timeout)."""
+    from mp_workers import migrate_rank
+
+    res = spawn_local_job(world, migrate_rank, kind, shrink_to, timeout=300)
+    assert len({tuple(r["seqs"]) for r in res}) == 1, [r["seqs"] for r in res]
+    assert len({tuple(sorted(r["epochs"].items())) for r in res}) == 1
+    assert sum(1 for r in res if not r["tiles_shrunk"]) == world - shrink_to
