@@ -71,14 +71,16 @@ def rank_body(rank, world, n, iters, planes):
         job.barrier()
         return (time.perf_counter() - t0) * 1e3, stats
 
-    out = {"glups": {}, "redistribute_ms": {}, "moved_bytes": {}}
+    out = {"glups": {}, "redistribute_ms": {}, "moved_bytes": {}, "stages": {}}
     job.run_bytes(blob)  # warm: kernels, graphs of the analysis cache, peer maps
     out["glups"]["initial_8"] = phase()
     ms, st = redistribute(world // 2)
     out["redistribute_ms"]["8->4"], out["moved_bytes"]["8->4"] = ms, st["bytes_in"]
+    out["stages"]["8->4"] = {k: st[k] for k in ("pull_ms", "barrier_free_ms", "peer_maps_ms")}
     out["glups"]["shrunk_4"] = phase()
     ms, st = redistribute(world)
     out["redistribute_ms"]["4->8"], out["moved_bytes"]["4->8"] = ms, st["bytes_in"]
+    out["stages"]["4->8"] = {k: st[k] for k in ("pull_ms", "barrier_free_ms", "peer_maps_ms")}
     out["glups"]["restored_8"] = phase()
     sample = {p: job.fetch(u, ((p, p + 1), (0, n), (0, n))) for p in planes}
     job.close()
@@ -127,7 +129,9 @@ def main():
                        "iterations_per_phase": it, "workers": [w, w // 2, w],
                        "placement": "worker i on GPU i mod visible GPUs"},
             "redistribute_ms": redist, "moved_gib": {k: v / 2 ** 30 for k, v in moved.items()},
-            "glups": glups, "bit_equal_to_unrescaled": same, "sample_planes": planes}
+            "glups": glups, "bit_equal_to_unrescaled": same, "sample_planes": planes,
+            "stage_ms_max_over_ranks": {d: {k: max(r["stages"][d][k] for r in per_rank)
+                                            for k in per_rank[0]["stages"][d]} for d in per_rank[0]["stages"]}}
     print(json.dumps(line), flush=True)
     return 0 if same else 1
 
