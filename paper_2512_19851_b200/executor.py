@@ -23,6 +23,7 @@ kernels actually launched and `device_ms` is CUDA-event time when requested.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -77,7 +78,7 @@ class GpuExecutor:
         self.transport = None        # peer transport when the job has >1 worker
         self.kernel_events: list = []
         self.graphs = True           # replay repeated batches as CUDA graphs
-        self.overlap = True          # defer push-plan peer pulls behind interior planes
+        self.overlap = os.environ.get("EST_OVERLAP", "1") == "1"  # defer peer pulls behind the interior
         self._analysis: dict = {}    # DAG key -> (metas, plans)
         self._launches: dict = {}    # (DAG key, node, layout version) -> launches
         self._recording = None
@@ -621,29 +622,52 @@ class GpuExecutor:
         else:
             self.dev.launch(kern, grid, params, COMPUTE)
 
-    def _zranges(self, zsplit, geom, rank: int, tile, ps, local, nz: int) -> list:
-        """Output-plane ranges to launch: all, or the part that reads only
-        interior planes ("interior") / the part that touches ghost planes."""
-        if zsplit is None or rank != 3:
-            return [(0, nz)]
+    def _subboxes(self, zsplit, geom, rank: int, tile, ps, local, n3) -> list:
+        """Sub-boxes (offset (z, y, x) within the box, extents) to launch: the
+        whole box, or the part whose stencil reads no ghost cells
+        ("interior") / the rest ("boundary"). Rank-3 slabs split along z only
+        (their neighbours are z-neighbours); rank-2 tiles split into the
+        interior rectangle and up to four border strips."""
+        whole = [((0, 0, 0), tuple(n3))]
+        if zsplit is None:
+            return whole
         rz = max(s[0][0] for s in geom["slots"])
-        ez = tile.buffers[ps.output].ext[0]
-        lo = min(nz, max(0, rz - local[0]))
-        hi = max(lo, min(nz, ez - rz - local[0]))
+        ry = max(s[0][1] for s in geom["slots"])
+        rx = max(s[0][2] for s in geom["slots"])
+        ext = tile.buffers[ps.output].ext
+        nz, ny, nx = n3
+        if rank == 3:
+            lz, ly, lx = local
+            r = ((max(0, rz - lz), min(nz, ext[0] - rz - lz)), (0, ny), (0, nx))
+        else:
+            ly, lx = local
+            r = ((0, nz), (max(0, ry - ly), min(ny, ext[1] - ry - ly)), (max(0, rx - lx), min(nx, ext[2] - rx - lx)))
+        (z0, z1), (y0, y1), (x0, x1) = r
+        empty = z1 <= z0 or y1 <= y0 or x1 <= x0
         if zsplit == "interior":
-            return [(lo, hi)] if hi > lo else []
-        if hi <= lo:
-            return [(0, nz)]
-        return [r for r in ((0, lo), (hi, nz)) if r[1] > r[0]]
+            return [] if empty else [((z0, y0, x0), (z1 - z0, y1 - y0, x1 - x0))]
+        if empty:
+            return whole
+        parts = [((0, 0, 0), (z0, ny, nx)), ((z1, 0, 0), (nz - z1, ny, nx)),          # z caps
+                 ((z0, 0, 0), (z1 - z0, y0, nx)), ((z0, y1, 0), (z1 - z0, ny - y1, nx)),  # y strips
+                 ((z0, y0, 0), (z1 - z0, y1 - y0, x0)), ((z0, y0, x1), (z1 - z0, y1 - y0, nx - x1))]
+        return [(o, n) for o, n in parts if min(n) > 0]
+
+    OVERLAP_RANKS = (3,)
 
     def overlap_eligible(self, plan) -> bool:
-        """Halo/compute overlap applies to single-tile rank-3 stream nodes."""
+        """Halo/compute overlap for single-tile stream nodes. Rank-3 slabs only
+        by default: their faces are whole planes (MBs over NVLink) and the
+        boundary launch is one plane per side; rank-2 halos are a few KB while
+        four border-strip launches cost more than they hide (measured:
+        profiles/r1s2_overlap_rank2.txt). `OVERLAP_RANKS` opts rank 2 in."""
         if len(self.store.tiles) != 1 or len(plan.statements) != 1:
             return False
         info = self.store.arrays[plan.statements[0].output]
-        if info.rank != 3:
+        if info.rank not in self.OVERLAP_RANKS:
             return False
-        return codegen.kernel_source_for(plan, 3, info.dtype, self.skeleton)[6].skeleton == "stream"
+        return all(codegen.kernel_source_for(plan, info.rank, info.dtype, self.skeleton, sm)[6].skeleton == "stream"
+                   for sm in ((False,) if info.rank == 3 else (False, True)))
 
     SPLIT_MIN_POINTS = 1 << 16
 
@@ -705,11 +729,10 @@ class GpuExecutor:
                 it["ipz"].append(ib.pz)
             if sig.skeleton == "stream":
                 local = [g - o for g, o in zip(g_lo, self.store.decomp.tile_origin(shape, tile.coords))]
-                for z_a, z_b in self._zranges(zsplit, geom, rank, tile, ps, local, n3[0]):
-                    sub = dict(it, out=it["out"] + z_a * out_buf.pz * out_buf.elem, nz=z_b - z_a)
-                    sub_local = list(local)
-                    if rank == 3:
-                        sub_local[0] += z_a
+                for (oz, oy, ox), (mz, my, mx) in self._subboxes(zsplit, geom, rank, tile, ps, local, n3):
+                    sub = dict(it, out=it["out"] + (oz * out_buf.pz + oy * out_buf.py + ox) * out_buf.elem,
+                               nz=mz, ny=my, nx=mx)
+                    sub_local = [l + o for l, o in zip(local, (oz, oy, ox)[3 - rank:])]
                     stream.item_geometry(sub, self.dev.sm_count, geom)
                     self._launch_stream(kern, sig, geom, sub, tile, ps, [sub_local])
                 continue

@@ -30,8 +30,9 @@ def test_rounds_and_handshake_across_processes(kind, world, odf, batch):
     assert len({r["seq"] for r in res if r["tiles"]}) == 1
     # net strips are symmetric: what ranks pulled equals what they counted
     assert sum(r["net"] for r in res) > 0
-    if kind == "heat3d":  # rank-3 slabs: halo pulls overlap interior planes on the copy lane
-        assert all(r["copy_lane_pulls"] > 0 for r in res)
+    # rank-3 slabs: halo pulls overlap the interior planes on the copy lane
+    if kind == "heat3d":
+        assert all(r["copy_lane_pulls"] > 0 for r in res if r["tiles"])
     tiles = sorted(t for r in res for t in r["tiles"])
     assert len(tiles) == len(set(tiles)) == world * odf
 
