@@ -96,11 +96,16 @@ def layout(st: StmtSig, dtype: int, cfg: StreamCfg):
     return slots, off, off + 8 * n_bars + 1024
 
 
-# rank-2 boxes below this many points (e.g. the 1024^2 C1 grid) use shorter
-# tiles so the grid still covers every SM
+# rank-2 boxes below this many points (e.g. the 1024^2 C1 grid) use smaller
+# tiles so the grid still covers every SM (64x16, 8 rows per thread: C1 sweep,
+# profiles/r1s2_c1_small_tiles.txt)
 SMALL_2D_POINTS = 8 << 20
-DEFAULT_2D_SMALL = StreamCfg(bx=128, by=16, ty=4, prefetch=3, persistent=True, ws=True, zreg=False,
-                             l2promo=2, v2=True)
+DEFAULT_2D_SMALL = StreamCfg(bx=int(os.environ.get("EST_STREAM2DS_BX", 64)),
+                             by=int(os.environ.get("EST_STREAM2DS_BY", 16)),
+                             ty=int(os.environ.get("EST_STREAM2DS_TY", 2)),
+                             prefetch=int(os.environ.get("EST_STREAM2DS_PREFETCH", 2)),
+                             persistent=os.environ.get("EST_STREAM2DS_PERSISTENT", "1") == "1",
+                             ws=True, zreg=False, l2promo=2, v2=True)
 
 
 def fallback_cfgs(rank: int, small: bool = False) -> list:
