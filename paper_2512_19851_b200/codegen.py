@@ -254,7 +254,7 @@ def kernel_source_for(plan, rank: int, dtype: int, skeleton: str = "auto", small
     """
     from . import stream
 
-    cfg = stream.cfg_for(rank, small)
+    cfg = stream.cfg_for(rank, small, dtype)
     key = (tuple(p.instructions for p in plan.statements), rank, dtype, skeleton, cfg)
     hit = _SRC_CACHE.get(key)
     if hit is not None:
@@ -262,7 +262,7 @@ def kernel_source_for(plan, rank: int, dtype: int, skeleton: str = "auto", small
     stmts = tuple(stmt_sig(p, rank) for p in plan.statements)
     skel = "point"
     if skeleton in ("auto", "stream"):
-        for c in stream.fallback_cfgs(rank, small):
+        for c in stream.fallback_cfgs(rank, small, dtype):
             if stream_eligible(stmts, rank, dtype, c):
                 skel, cfg = "stream", c
                 break

@@ -108,11 +108,11 @@ DEFAULT_2D_SMALL = StreamCfg(bx=int(os.environ.get("EST_STREAM2DS_BX", 64)),
                              ws=True, zreg=False, l2promo=2, v2=True)
 
 
-def fallback_cfgs(rank: int, small: bool = False) -> list:
+def fallback_cfgs(rank: int, small: bool = False, dtype: int = DTYPE_F64) -> list:
     """Configurations to try in order: the default, then shorter tiles, so
     multi-input statements whose rings do not fit the default tile's shared
     memory (e.g. cavity flow's 3-input momentum updates) still stream."""
-    first = cfg_for(rank, small)
+    first = cfg_for(rank, small, dtype)
     out = [first]
     for by in (16, 8, 4):
         if by < first.by:
@@ -122,18 +122,29 @@ def fallback_cfgs(rank: int, small: bool = False) -> list:
     return out
 
 
-def cfg_for(rank: int, small: bool = False) -> StreamCfg:
+# fp64 rank-2 tiles: 24 rows per thread (ty 2) beats the fp32 wave's 12
+# (Laplace 16384^2 fp64: 0.80 -> 0.90 of measured HBM; the fp32 wave falls
+# from 0.99 to 0.76 with ty 2 - profiles/r1s2_laplace16k_f64_sweep.txt)
+DEFAULT_2D_F64 = StreamCfg(bx=DEFAULT_2D.bx, by=DEFAULT_2D.by,
+                           ty=int(os.environ.get("EST_STREAM2D_TY_F64", 2)),
+                           prefetch=DEFAULT_2D.prefetch, persistent=True, ws=True, zreg=False,
+                           l2promo=2, v2=DEFAULT_2D.v2)
+
+
+def cfg_for(rank: int, small: bool = False, dtype: int = DTYPE_F64) -> StreamCfg:
     """Rank-3 nodes stream along z; rank-2 nodes run the same warp-specialised
     TMA pipeline on a (1, Y, X) view: every item is one (BY+2ry) x (BX+2rx)
     tile, and the persistent grid lets the producer prefetch the NEXT items'
     tiles while the current one is computed."""
     if rank == 3:
         return DEFAULT
-    return DEFAULT_2D_SMALL if small else DEFAULT_2D
+    if small:
+        return DEFAULT_2D_SMALL
+    return DEFAULT_2D_F64 if dtype == DTYPE_F64 else DEFAULT_2D
 
 
 def eligible(stmts, rank: int, dtype: int = DTYPE_F64, cfg: StreamCfg | None = None) -> bool:
-    cfg = cfg or cfg_for(rank)
+    cfg = cfg or cfg_for(rank, False, dtype)
     if rank not in (2, 3) or len(stmts) != 1 or stmts[0].arity == 0:
         return False
     if rank == 2 and not cfg.ws:
@@ -186,7 +197,7 @@ __device__ __forceinline__ void tma_load3(void* dst, const void* tm, int x, int 
 
 
 def source(sig: NodeSig, rank: int, cfg: StreamCfg | None = None) -> tuple:
-    cfg = cfg or cfg_for(rank)
+    cfg = cfg or cfg_for(rank, False, sig.dtype)
     if cfg.ws:
         return source_ws2(sig, rank, cfg) if cfg.v2 else source_ws(sig, rank, cfg)
     BX, BY, TY = cfg.bx, cfg.by, cfg.ty
