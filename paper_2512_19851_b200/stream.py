@@ -2,25 +2,26 @@
 
 For rank-3 single-statement nodes (the 3-D heat/Jacobi sweeps that dominate
 the BASELINE configs) every input element must cross HBM once and every
-output once (16 B per update in fp64). The skeleton:
+output once (16 B per update in fp64). Rank-2 nodes run the same pipeline on
+a (1, Y, X) view with one tile per work item. The generated kernel (ws2):
 
-* work item = a BX x BY column of the output box over ZCHUNK planes. Either
-  one CTA per item (`persistent=False`) or a persistent one-wave grid walking
-  items round-robin (x-tiles fastest) — both are kept because which one keeps
-  the shared halo rows in L2 is a measured property (profiles/);
-* per input slot s with z-radius rz a ring of 2*rz+1+PREFETCH shared-memory
-  stages holds one input plane tile plus its (ry, rx) halo; each stage is ONE
-  `cp.async.bulk.tensor.3d` (TMA) issued by a single elected thread and
-  completed on the stage's mbarrier (expect_tx). The TMA box starts at a
-  16-byte aligned x coordinate (a hardware requirement found with
+* work item = a BX x BY column of the output box over ZCHUNK planes (rank 2:
+  one tile); non-persistent grid for rank 3, persistent for rank 2;
+* a dedicated producer warp streams each input slot's planes (tile + halo)
+  with ONE `cp.async.bulk.tensor.3d` (TMA) per plane into a ring of
+  2*rz+1+PREFETCH shared-memory stages, gated by FULL (expect_tx) / EMPTY
+  (one arrive per compute warp) mbarriers. The TMA box starts at a 16-byte
+  aligned x coordinate (a hardware requirement found with
   scripts/probes/tma_probe.cu; the sub-16 B shift goes into the shared-memory
   column index);
-* every thread evaluates the postorder plan (codegen._emit_expr) for BY/TY
-  rows of the current plane from shared memory with compile-time offsets and
-  stores with coalesced st.global (x fastest);
-* after one CTA barrier the stage that fell out of the z-window is refilled
-  PREFETCH planes ahead. Fill counters run across items, so mbarrier phases
-  never need re-initialisation.
+* each compute thread owns BY/TY CONSECUTIVE output rows of one column: its
+  column of every slot with pure-z / centre operands lives in registers
+  (2rz+1 planes, rotated by unrolling the plane loop), in-plane (dy, 0)
+  operands of its own rows come from those registers, everything else from
+  the ring; the postorder plan is emitted by codegen._emit_expr (one rounded
+  IEEE op per plan instruction) and stored with coalesced st.global;
+* ring stages and phases are counters; fill counters run across items, so
+  mbarrier phases never need re-initialisation.
 """
 
 from __future__ import annotations
@@ -197,296 +198,15 @@ __device__ __forceinline__ void tma_load3(void* dst, const void* tm, int x, int 
 
 
 def source(sig: NodeSig, rank: int, cfg: StreamCfg | None = None) -> tuple:
+    """-> (source, kernel name, block, smem, items per launch, geometry).
+
+    Only the warp-specialised ws2 pipeline is generated; the earlier
+    variants (CTA-barrier rings, one row per thread, lockstep persistent
+    grids) are recorded with their measurements in profiles/r1_stream_sweep.md."""
     cfg = cfg or cfg_for(rank, False, sig.dtype)
-    if cfg.ws:
-        return source_ws2(sig, rank, cfg) if cfg.v2 else source_ws(sig, rank, cfg)
-    BX, BY, TY = cfg.bx, cfg.by, cfg.ty
-    st = sig.stmts[0]
-    T = CTYPE[sig.dtype]
-    elem = ELEM[sig.dtype]
-    q = 16 // elem
-    slots, data_bytes, smem = layout(st, sig.dtype, cfg)
-    n_in = st.arity
-    rpt = BY // TY
-    L = []
-    a = L.append
-    a(f'// generated by paper_2512_19851_b200/stream.py — skeleton "stream" (TMA 2.5-D) {cfg}')
-    a(f"typedef {T} T;")
-    a("struct __align__(64) Tmap { unsigned long long w[16]; };")
-    a(f"struct __align__(64) Params {{ Tmap tm[{n_in}];")
-    a("  unsigned long long out; long long opy, opz, nx, ny, nz, zc, nbx, nby, nzc;")
-    a(f"  long long cx0[{n_in}], cy0[{n_in}], cz0[{n_in}]; }};")
-    L.append(_PTX_HELPERS)
-    a(f'extern "C" __global__ void __launch_bounds__({BX * TY})')
-    a("est_stream(const __grid_constant__ Params p) {")
-    a("  extern __shared__ __align__(1024) unsigned char smem[];")
-    a(f"  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + {data_bytes});")
-    a("  const int tx = threadIdx.x, ty = threadIdx.y;")
-    a("  const bool leader = (tx == 0 && ty == 0);")
-    a("  const int nbx = (int)p.nbx, nby = (int)p.nby;")
-    a("  const int n_items = nbx * nby * (int)p.nzc;")
-    bar = 0
-    for s, (_r, _wh, stages, _pl, off) in enumerate(slots):
-        a(f"  unsigned long long* bar{s} = bars + {bar};")
-        a(f"  const {T}* ring{s} = reinterpret_cast<const {T}*>(smem + {off});")
-        a(f"  int fill{s} = 0;  // planes loaded into ring {s} so far (all items)")
-        bar += stages
-    a("  if (leader) {")
-    for s in range(n_in):
-        a(f"    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm[{s}]) : \"memory\");")
-    a(f"    for (int i = 0; i < {bar}; ++i) mbar_init(bars + i, 1);")
-    a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
-    a("  }")
-    a("  __syncthreads();")
-    a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
-    a("    const int bx = item % nbx, rest = item / nbx;")
-    a("    const int by = rest % nby, bzc = rest / nby;")
-    a(f"    const int x0 = bx * {BX}, y0 = by * {BY};")
-    a("    const int zs = bzc * (int)p.zc;")
-    a("    const int nzl = ((zs + (int)p.zc) < (int)p.nz ? (int)p.zc : (int)p.nz - zs);")
-    for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
-        a(f"    const int xs{s} = (int)p.cx0[{s}] + x0 - {rx};")
-        a(f"    const int sh{s} = xs{s} & {q - 1};  // TMA x start must be 16-byte aligned")
-        a(f"    auto load{s} = [&](int k) {{  // k-th input plane of this item (q = k - rz)")
-        a(f"      const int g = fill{s} + k; const int stg = g % {stages};")
-        a(f"      mbar_expect(bar{s} + stg, {w * h * elem});")
-        a(f"      tma_load3(smem + {off} + stg * {plane}, &p.tm[{s}], xs{s} - sh{s},"
-          f" (int)p.cy0[{s}] + y0 - {ry}, (int)p.cz0[{s}] + zs + k - {rz}, bar{s} + stg);")
-        a("    };")
-    a("    if (leader) {")
-    a("      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");")
-    for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
-        a(f"      for (int k = 0; k < {stages} && k < nzl + {2 * rz}; ++k) load{s}(k);")
-    a("    }")
-    a(f"    T* __restrict__ orow = reinterpret_cast<T*>(p.out) + (long long)zs * p.opz"
-      f" + (long long)(y0 + ty) * p.opy + (x0 + tx);")
-    a("    const bool colok = (x0 + tx) < (int)p.nx;")
-    a("    for (int z = 0; z < nzl; ++z) {")
-    for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
-        a("      if (z == 0) {")
-        a(f"        for (int k = 0; k <= {2 * rz}; ++k) {{ const int g = fill{s} + k;"
-          f" mbar_wait(bar{s} + g % {stages}, (g / {stages}) & 1); }}")
-        a("      } else {")
-        a(f"        const int g = fill{s} + z + {2 * rz}; mbar_wait(bar{s} + g % {stages}, (g / {stages}) & 1);")
-        a("      }")
-    used: dict = {}
-    for ins in st.instructions:
-        if ins[0] == "load":
-            used.setdefault(ins[1], set()).add(ins[2][0])
-    for s, dzs in sorted(used.items()):
-        (rz, ry, rx), (w, h), stages, plane, off = slots[s]
-        for dz in sorted(dzs):
-            nm = f"P{s}_{'m' if dz < 0 else 'p'}{abs(dz)}"
-            a(f"      const {T}* {nm} = ring{s} + ((fill{s} + z + {rz + dz}) % {stages}) * {plane // elem}"
-              f" + ty * {w} + tx + sh{s};")
-
-    def load(slot, off3):
-        dz, dy, dx = off3
-        (rz, ry, rx), (w, h), _stg, _pl, _o = slots[slot]
-        nm = f"P{slot}_{'m' if dz < 0 else 'p'}{abs(dz)}"
-        return f"{nm}[r * {TY * w} + {(ry + dy) * w + (rx + dx)}]"
-
-    lines, res = _emit_expr(st, sig.dtype, load)
-    a("      #pragma unroll")
-    a(f"      for (int r = 0; r < {rpt}; ++r) {{")
-    a(f"        if (colok && (y0 + ty + r * {TY}) < (int)p.ny) {{")
-    for ln in lines:
-        a("          " + ln)
-    a(f"          orow[(long long)r * {TY} * p.opy] = {res};")
-    a("        }")
-    a("      }")
-    a("      orow += p.opz;")
-    a("      __syncthreads();  // every thread is done with plane z - rz of every ring")
-    a("      if (leader) {")
-    a("        asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");")
-    for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
-        a(f"        if (z + {stages} < nzl + {2 * rz}) load{s}(z + {stages});")
-    a("      }")
-    a("    }")
-    for s, ((rz, _ry, _rx), _wh, _stages, _pl, _off) in enumerate(slots):
-        a(f"    fill{s} += nzl + {2 * rz};")
-    a("  }")
-    a("}")
-    src = "\n".join(L) + "\n"
-    return src, "est_stream", (BX, TY, 1), smem, 1, {"slots": slots, "smem": smem, "cfg": cfg}
-
-
-def source_ws(sig: NodeSig, rank: int, cfg: StreamCfg) -> tuple:
-    """Warp-specialised variant: one producer warp (lane 0) streams planes with
-    TMA through FULL (expect_tx) / EMPTY (one arrive per compute warp)
-    mbarriers per ring stage; compute warps never meet at a CTA barrier and run
-    ahead into the next item while the producer keeps PREFETCH planes in
-    flight. With `zreg` each thread keeps its own column's pure-z operands
-    (offsets (dz,0,0)) in registers, rotating one plane per step."""
-    BX, BY, TY = cfg.bx, cfg.by, cfg.ty
-    st = sig.stmts[0]
-    T = CTYPE[sig.dtype]
-    elem = ELEM[sig.dtype]
-    q = 16 // elem
-    slots, data_bytes, smem = layout(st, sig.dtype, cfg)
-    n_in = st.arity
-    rpt = BY // TY
-    CT = BX * TY
-    NW = CT // 32
-    assert CT % 32 == 0
-    loads = [ins for ins in st.instructions if ins[0] == "load"]
-    zreg_slots = set()
-    if cfg.zreg:
-        for s in range(n_in):
-            if any(i[1] == s and i[2][1] == 0 and i[2][2] == 0 for i in loads):
-                zreg_slots.add(s)
-    L = []
-    a = L.append
-    a(f'// generated by paper_2512_19851_b200/stream.py — skeleton "stream" (TMA 2.5-D, warp-specialised) {cfg}')
-    a(f"typedef {T} T;")
-    a("struct __align__(64) Tmap { unsigned long long w[16]; };")
-    a(f"struct __align__(64) Params {{ Tmap tm[{n_in}];")
-    a("  unsigned long long out; long long opy, opz, nx, ny, nz, zc, nbx, nby, nzc;")
-    a(f"  long long cx0[{n_in}], cy0[{n_in}], cz0[{n_in}]; }};")
-    L.append(_PTX_HELPERS)
-    a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
-    a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
-    a(f'extern "C" __global__ void __launch_bounds__({CT + 32})')
-    a("est_stream(const __grid_constant__ Params p) {")
-    a("  extern __shared__ __align__(1024) unsigned char smem[];")
-    a(f"  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + {data_bytes});")
-    a("  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;")
-    a("  const int nbx = (int)p.nbx, nby = (int)p.nby;")
-    a("  const int n_items = nbx * nby * (int)p.nzc;")
-    nb = 0
-    for s, (_r, _wh, stages, _pl, off) in enumerate(slots):
-        a(f"  unsigned long long* full{s} = bars + {nb};")
-        a(f"  unsigned long long* empty{s} = bars + {nb + stages};")
-        a(f"  const {T}* ring{s} = reinterpret_cast<const {T}*>(smem + {off});")
-        nb += 2 * stages
-    a("  if (tid == 0) {")
-    for s, (_r, _wh, stages, _pl, _off) in enumerate(slots):
-        a(f"    for (int i = 0; i < {stages}; ++i) {{ mbar_init(full{s} + i, 1); mbar_init(empty{s} + i, {NW}); }}")
-    a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
-    a("  }")
-    a("  __syncthreads();")
-    # ---------------- producer warp
-    a(f"  if (warp == {NW}) {{")
-    a("    if (lane != 0) return;")
-    for s in range(n_in):
-        a(f"    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm[{s}]) : \"memory\");")
-    for s in range(n_in):
-        a(f"    int fill{s} = 0;")
-    a("    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
-    a("      const int bx = item % nbx, rest = item / nbx;")
-    a("      const int by = rest % nby, bzc = rest / nby;")
-    a(f"      const int x0 = bx * {BX}, y0 = by * {BY};")
-    a("      const int zs = bzc * (int)p.zc;")
-    a("      const int nzl = ((zs + (int)p.zc) < (int)p.nz ? (int)p.zc : (int)p.nz - zs);")
-    # Issue planes in the order the consumers NEED them: output z needs plane
-    # k = z + 2*rz of slot s (all of k <= 2*rz at z == 0). Issuing slot by slot
-    # in plain k order would deadlock when a later slot has the larger radius
-    # (the producer would block on an EMPTY slot whose release needs a plane it
-    # has not issued yet).
-    a("      for (int t = 0; t < nzl; ++t) {")
-    for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
-        a(f"        for (int k = (t == 0 ? 0 : t + {2 * rz}); k <= t + {2 * rz}; ++k) {{")
-        a(f"          const int g = fill{s} + k, stg = g % {stages};")
-        a(f"          if (g >= {stages}) mbar_wait(empty{s} + stg, ((g / {stages}) - 1) & 1);")
-        a(f"          const int xs = (int)p.cx0[{s}] + x0 - {rx};")
-        a(f"          mbar_expect(full{s} + stg, {w * h * elem});")
-        a(f"          tma_load3(smem + {off} + stg * {plane}, &p.tm[{s}], xs - (xs & {q - 1}),"
-          f" (int)p.cy0[{s}] + y0 - {ry}, (int)p.cz0[{s}] + zs + k - {rz}, full{s} + stg);")
-        a("        }")
-    a("      }")
-    for s, ((rz, _ry, _rx), _wh, _stg, _pl, _off) in enumerate(slots):
-        a(f"      fill{s} += nzl + {2 * rz};")
-    a("    }")
-    a("    return;")
-    a("  }")
-    # ---------------- compute warps
-    a(f"  const int tx = tid % {BX}, ty = tid / {BX};")
-    for s in range(n_in):
-        a(f"  int fill{s} = 0;")
-    for s in sorted(zreg_slots):
-        rz = slots[s][0][0]
-        a(f"  T cz{s}[{rpt}][{2 * rz + 1}];")
-    a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
-    a("    const int bx = item % nbx, rest = item / nbx;")
-    a("    const int by = rest % nby, bzc = rest / nby;")
-    a(f"    const int x0 = bx * {BX}, y0 = by * {BY};")
-    a("    const int zs = bzc * (int)p.zc;")
-    a("    const int nzl = ((zs + (int)p.zc) < (int)p.nz ? (int)p.zc : (int)p.nz - zs);")
-    for s, ((rz, ry, rx), (w, h), stages, plane, off) in enumerate(slots):
-        a(f"    const int sh{s} = ((int)p.cx0[{s}] + x0 - {rx}) & {q - 1};")
-    a(f"    T* __restrict__ orow = reinterpret_cast<T*>(p.out) + (long long)zs * p.opz"
-      f" + (long long)(y0 + ty) * p.opy + (x0 + tx);")
-    a("    const bool colok = (x0 + tx) < (int)p.nx;")
-    a("    for (int z = 0; z < nzl; ++z) {")
-    for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
-        a("      if (z == 0) {")
-        a(f"        for (int k = 0; k <= {2 * rz}; ++k) {{ const int g = fill{s} + k;"
-          f" mbar_wait(full{s} + g % {stages}, (g / {stages}) & 1); }}")
-        a("      } else {")
-        a(f"        const int g = fill{s} + z + {2 * rz}; mbar_wait(full{s} + g % {stages}, (g / {stages}) & 1);")
-        a("      }")
-    need: dict = {}
-    for ins in loads:
-        s, (dz, dy, dx) = ins[1], ins[2]
-        if s in zreg_slots and dy == 0 and dx == 0:
-            continue
-        need.setdefault(s, set()).add(dz)
-    for s in zreg_slots:
-        rz = slots[s][0][0]
-        need.setdefault(s, set()).update(range(-rz, rz + 1))  # register fill at z == 0 + newest plane
-    for s, dzs in sorted(need.items()):
-        (rz, ry, rx), (w, h), stages, plane, off = slots[s]
-        for dz in sorted(dzs):
-            nm = f"P{s}_{'m' if dz < 0 else 'p'}{abs(dz)}"
-            a(f"      const {T}* {nm} = ring{s} + ((fill{s} + z + {rz + dz}) % {stages}) * {plane // elem}"
-              f" + ty * {w} + tx + sh{s};")
-    for s in sorted(zreg_slots):
-        (rz, ry, rx), (w, h), _stg, _pl, _o = slots[s]
-        ctr = ry * w + rx
-        a("      #pragma unroll")
-        a(f"      for (int r = 0; r < {rpt}; ++r) {{")
-        a("        if (z == 0) {")
-        for dz in range(-rz, rz):
-            nm = f"P{s}_{'m' if dz < 0 else 'p'}{abs(dz)}"
-            a(f"          cz{s}[r][{dz + rz}] = {nm}[r * {TY * w} + {ctr}];")
-        a("        }")
-        nm = f"P{s}_p{rz}" if rz > 0 else f"P{s}_p0"
-        a(f"        cz{s}[r][{2 * rz}] = {nm}[r * {TY * w} + {ctr}];")
-        a("      }")
-
-    def load(slot, off3):
-        dz, dy, dx = off3
-        (rz, ry, rx), (w, h), _stg, _pl, _o = slots[slot]
-        if slot in zreg_slots and dy == 0 and dx == 0:
-            return f"cz{slot}[r][{dz + rz}]"
-        nm = f"P{slot}_{'m' if dz < 0 else 'p'}{abs(dz)}"
-        return f"{nm}[r * {TY * w} + {(ry + dy) * w + (rx + dx)}]"
-
-    lines, res = _emit_expr(st, sig.dtype, load)
-    a("      #pragma unroll")
-    a(f"      for (int r = 0; r < {rpt}; ++r) {{")
-    a(f"        if (colok && (y0 + ty + r * {TY}) < (int)p.ny) {{")
-    for ln in lines:
-        a("          " + ln)
-    a(f"          orow[(long long)r * {TY} * p.opy] = {res};")
-    a("        }")
-    for s in sorted(zreg_slots):
-        rz = slots[s][0][0]
-        for d in range(2 * rz):
-            a(f"        cz{s}[r][{d}] = cz{s}[r][{d + 1}];")
-    a("      }")
-    a("      orow += p.opz;")
-    a("      __syncwarp();")
-    for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
-        a(f"      if (lane == 0) mbar_arrive(empty{s} + (fill{s} + z) % {stages});  // plane k = z is dead")
-    a("    }")
-    for s, ((rz, _ry, _rx), _wh, stages, _pl, _off) in enumerate(slots):
-        a(f"    for (int k = nzl; k < nzl + {2 * rz}; ++k) if (lane == 0) mbar_arrive(empty{s} + (fill{s} + k) % {stages});")
-        a(f"    fill{s} += nzl + {2 * rz};")
-    a("  }")
-    a("}")
-    src = "\n".join(L) + "\n"
-    return src, "est_stream", (CT + 32, 1, 1), smem, 1, {"slots": slots, "smem": smem, "cfg": cfg}
+    if not (cfg.ws and cfg.v2):
+        raise ValueError("only the warp-specialised ws2 stream skeleton is generated")
+    return source_ws2(sig, rank, cfg)
 
 
 def source_ws2(sig: NodeSig, rank: int, cfg: StreamCfg) -> tuple:

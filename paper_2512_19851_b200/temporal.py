@@ -13,7 +13,7 @@ Every point is still computed by the same generated expression
 contraction), so results are bit-identical to K separate sweeps. Epochs,
 rounds and launch counts are kept per node by the executor.
 
-Kernel structure (warp-specialised like stream.source_ws):
+Kernel structure (warp-specialised like stream.source_ws2):
 * work item = a BX x BY output column of S over ZC planes; step j (1..K) of
   the chain covers the item tile expanded by (K-j)*r in y/x (overlapped
   tiling) and trails step j-1 by rz planes in z;
