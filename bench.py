@@ -159,7 +159,7 @@ def cpu_sample(w, iters: int = 2, planes: int = 34, threads: int = 0) -> dict:
     """Strict-order C oracle on a bounded sample of the workload, all host cores."""
     from oracle.oracle import _lib as olib, strict_eval_statement
     from paper_2512_19851_b200.analysis import compile_plan
-    from paper_2512_19851_b200.programs import DagProgram, heat3d_program, laplace_program, wave2d_program
+    from paper_2512_19851_b200.programs import DagProgram, heat3d_program, laplace_program
     from paper_2512_19851_b200.wire import DTYPE_F32
 
     n = w["n"]
@@ -297,7 +297,6 @@ def main():
     if world > 1:
         import torch.distributed as dist  # plumbing only: barrier + max-over-ranks
         dist.init_process_group("gloo")
-    from paper_2512_19851_b200.wire import decode_dag
 
     job, prog, arrays = build_job(w, world, rank, args.skeleton)
     blob = step_dag(w, prog.shapes, prog.dtypes, arrays)
@@ -359,7 +358,6 @@ def main():
     value = lups_step * args.steps / (dev_ms / 1e3) / 1e9
 
     # ---- end-to-end through the public API ------------------------------------
-    from paper_2512_19851_b200.device import PinnedBuffer
     plane_bounds = None
     shape = prog.shapes[arrays[0]]
     mid = shape[0] // 2

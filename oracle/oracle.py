@@ -30,13 +30,7 @@ import os
 
 import numpy as np
 
-from paper_2512_19851_b200.analysis import (
-    OP_BINARY,
-    OP_CONST,
-    OP_LOAD,
-    OP_UNARY,
-    compile_plan,
-)
+from paper_2512_19851_b200.analysis import OP_CONST, OP_LOAD, compile_plan
 from paper_2512_19851_b200.ir import Binary, Const, SlotRef, Unary
 from paper_2512_19851_b200.wire import DTYPE_F32, DTYPE_F64
 

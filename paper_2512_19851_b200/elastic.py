@@ -35,7 +35,6 @@ from .tiles import (
     GpuTile,
     TileBuffer,
     blob_header,
-    pad3,
     parse_blob_header,
 )
 

@@ -40,8 +40,6 @@ def host_logic_rank(rank, world, kind, odf, batch):
     from fakedev import FakeDevice
 
     ipc.Device = lambda device=0: FakeDevice(device, tag=f"r{rank}")
-    from paper_2512_19851_b200.analysis import analyze_dag
-
     prog, _ = _program(kind)
     job = ipc.IpcGpuJob(rank, world, odf=odf)
     for aid in sorted(prog.shapes):

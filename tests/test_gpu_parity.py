@@ -11,7 +11,7 @@ from golden_cases import case_names, get_case
 from oracle.oracle import (
     bits_equal, heat3d_reference, laplace_reference, reference_execute_dag, strict_execute_dag)
 from paper_2512_19851_b200.errors import MalformedDag, OffsetExceedsTileWidth
-from paper_2512_19851_b200.ir import Dag, DagNode, Statement, compute_edges, cst, ref
+from paper_2512_19851_b200.ir import Dag, DagNode, compute_edges, cst, ref
 from paper_2512_19851_b200.programs import (
     DagProgram, heat3d_program, laplace_program, wave2d_program)
 from paper_2512_19851_b200.session import GpuJob, run_program
