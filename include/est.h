@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define EST_ABI_VERSION 5
+#define EST_ABI_VERSION 6
 
 typedef struct est_ctx est_ctx;       /* one device + compute/copy streams      */
 typedef struct est_module est_module; /* an NVRTC-compiled, loaded cubin        */
@@ -83,6 +83,14 @@ int est_module_load_cubin(est_ctx *ctx, const void *image, est_module **out);
 int est_module_kernel(est_module *mod, const char *name, uint64_t *fn);
 int est_module_destroy(est_module *mod);
 int est_kernel_set_smem(uint64_t fn, int bytes);
+/* est_launch with flags: EST_LAUNCH_PDL = programmatic dependent launch (the
+ * kernel may be scheduled while the previous kernel on the stream drains; it
+ * must execute griddepcontrol.wait before touching memory that kernel wrote
+ * or reads - every generated skeleton does; replaces the per-node launch gap
+ * of executor.py:320-324's statement-at-a-time loop) */
+#define EST_LAUNCH_PDL 1
+int est_launch_ex(est_ctx *ctx, uint64_t fn, const uint32_t grid[3], const uint32_t block[3],
+                  uint32_t smem, const void *params, uint32_t params_size, int stream, int flags);
 /* resident CTAs per SM for a launch shape (persistent grids with grid-wide
  * barriers size themselves with it: every CTA must be co-resident) */
 int est_kernel_occupancy(uint64_t fn, int block, int smem, int *blocks_per_sm);

@@ -14,7 +14,7 @@ from .errors import from_code
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libest.so")
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 u64, i64, i32, u32 = C.c_uint64, C.c_int64, C.c_int, C.c_uint32
 vp = C.c_void_p
@@ -51,6 +51,7 @@ _SIGS = {
     "est_kernel_set_smem": (i32, [u64, i32]),
     "est_kernel_occupancy": (i32, [u64, i32, i32, C.POINTER(C.c_int)]),
     "est_launch": (i32, [vp, u64, P(u32), P(u32), u32, vp, u32, i32]),
+    "est_launch_ex": (i32, [vp, u64, P(u32), P(u32), u32, vp, u32, i32, i32]),
     "est_graph_begin": (i32, [vp, i32]),
     "est_graph_end": (i32, [vp, i32, P(vp)]),
     "est_graph_launch": (i32, [vp, vp, i32]),

@@ -198,6 +198,8 @@ typedef {T} T;
 {_param_decls(max_in, n_items)}
 extern "C" __global__ void __launch_bounds__({block[0] * block[1]})
 est_node(const __grid_constant__ Params p) {{
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic launch: predecessor complete
   long long b = blockIdx.x;
   int k = 0;
   while (k + 1 < p.n && b >= p.it[k + 1].blk0) ++k;

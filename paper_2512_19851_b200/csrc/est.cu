@@ -72,6 +72,7 @@ struct Driver {
     decltype(&cuLaunchKernel) launchKernel = nullptr;
     decltype(&cuFuncSetAttribute) funcSetAttribute = nullptr;
     decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) occupancy = nullptr;
+    decltype(&cuLaunchKernelEx) launchKernelEx = nullptr;
     bool ok = false;
 };
 static Driver g_drv;
@@ -99,6 +100,7 @@ static int driver() {
     rc |= resolve("cuFuncSetAttribute", g_drv.funcSetAttribute);
     rc |= resolve("cuTensorMapEncodeTiled", g_drv.tensorMapEncodeTiled);
     rc |= resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", g_drv.occupancy);
+    rc |= resolve("cuLaunchKernelEx", g_drv.launchKernelEx);
     if (rc) return 1;
     g_drv.ok = true;
     return 0;
@@ -490,6 +492,33 @@ extern "C" int est_launch(est_ctx *c, uint64_t fn, const uint32_t grid[3], const
                      CU_LAUNCH_PARAM_BUFFER_SIZE, &sz, CU_LAUNCH_PARAM_END};
     CU_TRY(g_drv.launchKernel((CUfunction)(uintptr_t)fn, grid[0], grid[1], grid[2], block[0],
                               block[1], block[2], smem, (CUstream)pick(c, s), nullptr, extra));
+    return 0;
+}
+
+extern "C" int est_launch_ex(est_ctx *c, uint64_t fn, const uint32_t grid[3], const uint32_t block[3],
+                             uint32_t smem, const void *params, uint32_t params_size, int s, int flags) {
+    if (!(flags & EST_LAUNCH_PDL)) return est_launch(c, fn, grid, block, smem, params, params_size, s);
+    if ((uint64_t)grid[0] * grid[1] * grid[2] == 0) return 0;
+    if (driver()) return 1;
+    CUDA_TRY(cudaSetDevice(c->device));
+    size_t sz = params_size;
+    void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void *>(params),
+                     CU_LAUNCH_PARAM_BUFFER_SIZE, &sz, CU_LAUNCH_PARAM_END};
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg = {};
+    cfg.gridDimX = grid[0];
+    cfg.gridDimY = grid[1];
+    cfg.gridDimZ = grid[2];
+    cfg.blockDimX = block[0];
+    cfg.blockDimY = block[1];
+    cfg.blockDimZ = block[2];
+    cfg.sharedMemBytes = smem;
+    cfg.hStream = (CUstream)pick(c, s);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CU_TRY(g_drv.launchKernelEx(&cfg, (CUfunction)(uintptr_t)fn, nullptr, extra));
     return 0;
 }
 

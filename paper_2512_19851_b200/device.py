@@ -97,11 +97,17 @@ class Graph:
             self.ptr = C.c_void_p()
 
 
-class Kernel:
-    __slots__ = ("fn", "name", "block", "smem")
+# programmatic dependent launch for kernels that wait on their predecessor
+# themselves (griddepcontrol.wait in the generated source)
+PDL = os.environ.get("EST_PDL", "1") == "1"
 
-    def __init__(self, fn: int, name: str, block, smem: int):
+
+class Kernel:
+    __slots__ = ("fn", "name", "block", "smem", "pdl")
+
+    def __init__(self, fn: int, name: str, block, smem: int, pdl: bool = False):
         self.fn, self.name, self.block, self.smem = fn, name, tuple(block), smem
+        self.pdl = pdl
 
 
 class Device:
@@ -183,7 +189,7 @@ class Device:
         check(self.lib.est_module_kernel(mod, name.encode(), C.byref(fn)))
         if smem > 48 * 1024:
             check(self.lib.est_kernel_set_smem(fn.value, smem))
-        k = Kernel(fn.value, name, block, smem)
+        k = Kernel(fn.value, name, block, smem, pdl=PDL and "griddepcontrol.wait" in source)
         self._kernels[key] = k
         return k
 
@@ -197,7 +203,10 @@ class Device:
     def launch(self, k: Kernel, grid, params: bytes, stream: int = COMPUTE) -> None:
         g = (C.c_uint32 * 3)(*grid)
         b = (C.c_uint32 * 3)(*k.block)
-        check(self.lib.est_launch(self.ctx, k.fn, g, b, k.smem, params, len(params), stream))
+        if k.pdl:
+            check(self.lib.est_launch_ex(self.ctx, k.fn, g, b, k.smem, params, len(params), stream, 1))
+        else:
+            check(self.lib.est_launch(self.ctx, k.fn, g, b, k.smem, params, len(params), stream))
         self.launches += 1
 
     # -- CUDA graphs ----------------------------------------------------------

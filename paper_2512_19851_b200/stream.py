@@ -266,12 +266,14 @@ def source_ws2(sig: NodeSig, rank: int, cfg: StreamCfg) -> tuple:
         a(f"  unsigned long long* full{s_} = bars + {nb};")
         a(f"  unsigned long long* empty{s_} = bars + {nb + stages};")
         nb += 2 * stages
+    a("  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");  // next node may be scheduled")
     a("  if (tid == 0) {")
     for s_, (_r, _wh, stages, _pl, _off) in enumerate(slots):
         a(f"    for (int i = 0; i < {stages}; ++i) {{ mbar_init(full{s_} + i, 1); mbar_init(empty{s_} + i, {NW}); }}")
     a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
     a("  }")
     a("  __syncthreads();")
+    a("  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");  // previous node's writes visible, its reads done")
     # ---------------- producer warp (identical issue order to source_ws)
     a(f"  if (warp == {NW}) {{")
     a("    if (lane != 0) return;")
