@@ -200,10 +200,13 @@ class Device:
                                             C.byref(n)))
         return n.value
 
-    def launch(self, k: Kernel, grid, params: bytes, stream: int = COMPUTE) -> None:
+    def launch(self, k: Kernel, grid, params: bytes, stream: int = COMPUTE, pdl: bool = True) -> None:
+        """`pdl`: the caller allows programmatic dependent launch here (no
+        cross-stream / cross-process event waits interleaved with the
+        predecessor kernel)."""
         g = (C.c_uint32 * 3)(*grid)
         b = (C.c_uint32 * 3)(*k.block)
-        if k.pdl:
+        if pdl and k.pdl:
             check(self.lib.est_launch_ex(self.ctx, k.fn, g, b, k.smem, params, len(params), stream, 1))
         else:
             check(self.lib.est_launch(self.ctx, k.fn, g, b, k.smem, params, len(params), stream))

@@ -429,7 +429,7 @@ class GpuExecutor:
         rec = self._launches.get(ck) if ck is not None else None
         if rec is not None and not self.time_kernels:
             for kern, grid, params in rec:
-                self.dev.launch(kern, grid, params, COMPUTE)
+                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
             return
         sig = codegen.stmt_sig(ps, 3)
         src, name, block, smem, wgeo = wavefront.source(sig, info.dtype, cfg)
@@ -463,7 +463,7 @@ class GpuExecutor:
         rec = self._launches.get(ck) if ck is not None else None
         if rec is not None and not self.time_kernels:
             for kern, grid, params in rec:
-                self.dev.launch(kern, grid, params, COMPUTE)
+                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
             return
         sig = codegen.stmt_sig(ps, info.rank)
         src, name, block, smem, geo = resident.source(sig, info.dtype, info.rank)
@@ -523,7 +523,7 @@ class GpuExecutor:
         rec = self._launches.get(ck) if ck is not None else None
         if rec is not None and not self.time_kernels:
             for kern, grid, params in rec:
-                self.dev.launch(kern, grid, params, COMPUTE)
+                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
             return
         src_buf, dst_buf = (home, twin) if ch % 2 == 0 else (twin, home)
         sig = codegen.stmt_sig(ps, 3)
@@ -597,7 +597,7 @@ class GpuExecutor:
         recorded = self._launches.get(ck) if ck is not None else None
         if recorded is not None and not self.time_kernels:
             for kern, grid, params in recorded:
-                self.dev.launch(kern, grid, params, COMPUTE)
+                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
             return
         self._recording = [] if ck is not None else None
         try:
@@ -616,11 +616,11 @@ class GpuExecutor:
         if self.time_kernels:
             ev0, ev1 = self.dev.event(), self.dev.event()
             ev0.record(COMPUTE)
-            self.dev.launch(kern, grid, params, COMPUTE)
+            self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
             ev1.record(COMPUTE)
             self.kernel_events.append((ev0, ev1, tag))
         else:
-            self.dev.launch(kern, grid, params, COMPUTE)
+            self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
 
     def _subboxes(self, zsplit, geom, rank: int, tile, ps, local, n3) -> list:
         """Sub-boxes (offset (z, y, x) within the box, extents) to launch: the
