@@ -9,10 +9,14 @@ process, so a long-lived per-GPU daemon owns the memory). This daemon:
   FREE 252 / PING 253 / STATS 254, replies D_OK 255 / D_ERR 256), so host
   blobs still work;
 * adds device allocations (additive kinds): DEV_ALLOC 257 {nbytes, meta} ->
-  u64 id + 64-byte CUDA IPC handle; DEV_OPEN 258 id -> handle + meta;
-  DEV_FREE 259 id. A worker checkpoints by copying its tile interiors
-  device-to-device into an IPC-mapped daemon allocation (no host round trip);
-  the restarted worker maps the same handle and copies back, then frees.
+  u64 id + 64-byte CUDA IPC handle of the ARENA holding it + u64 offset + u64
+  arena serial; DEV_OPEN 258 id -> the same + meta; DEV_FREE 259 id. A worker
+  checkpoints by copying its tile interiors device-to-device into the
+  IPC-mapped arena (no host round trip); the restarted worker maps the arena
+  once and copies back, then frees. Allocations are carved out of a few large
+  arenas (first fit, coalescing free list) that live as long as the daemon,
+  so a rescale pays one cudaMalloc / cudaIpcOpenMemHandle per arena instead
+  of one per (tile, array).
 
 One daemon per GPU slot, registered with the coordinator as role "daemon".
 """
@@ -33,6 +37,43 @@ from .wire import REGISTER, recv_frame, send_frame, send_json
 D_STORE, D_RETRIEVE, D_FREE, D_PING, D_STATS, D_OK, D_ERR = 250, 251, 252, 253, 254, 255, 256
 D_DEV_ALLOC, D_DEV_OPEN, D_DEV_FREE = 257, 258, 259
 _U64 = struct.Struct("<Q")
+ARENA_MIN = int(os.environ.get("EST_DAEMON_ARENA_BYTES", 2 << 30))
+ARENA_ALIGN = 1 << 16
+
+
+class _Arena:
+    """One exported device allocation; sub-allocations by offset."""
+
+    serials = iter(range(1, 1 << 62))
+
+    def __init__(self, dev, size: int):
+        self.ptr = dev.alloc(size)
+        dev.sync()
+        self.size = size
+        self.handle = dev.ipc_handle(self.ptr)
+        self.serial = next(_Arena.serials)
+        self.free = [(0, size)]  # sorted (offset, size)
+
+    def take(self, n: int):
+        for k, (off, sz) in enumerate(self.free):
+            if sz >= n:
+                if sz == n:
+                    del self.free[k]
+                else:
+                    self.free[k] = (off + n, sz - n)
+                return off
+        return None
+
+    def give(self, off: int, n: int) -> None:
+        self.free.append((off, n))
+        self.free.sort()
+        merged = []
+        for o, z in self.free:
+            if merged and merged[-1][0] + merged[-1][1] == o:
+                merged[-1] = (merged[-1][0], merged[-1][1] + z)
+            else:
+                merged.append((o, z))
+        self.free = merged
 
 
 class GpuMemoryDaemon:
@@ -44,7 +85,8 @@ class GpuMemoryDaemon:
         self._lock = threading.Lock()
         self._next = 1
         self._blobs: dict = {}
-        self._dev: dict = {}  # id -> (ptr, nbytes, handle, meta)
+        self._dev: dict = {}  # id -> (arena, offset, reserved bytes, nbytes, meta)
+        self._arenas: list = []
         daemon = self
 
         class Handler(socketserver.BaseRequestHandler):
@@ -88,21 +130,29 @@ class GpuMemoryDaemon:
         elif kind == D_STATS:
             with self._lock:
                 n = len(self._blobs) + len(self._dev)
-                total = sum(len(b) for b in self._blobs.values()) + sum(v[1] for v in self._dev.values())
+                total = sum(len(b) for b in self._blobs.values()) + sum(v[3] for v in self._dev.values())
             send_frame(sock, D_OK, struct.pack("<QQ", n, total))
         elif kind == D_DEV_ALLOC:
             req = json.loads(body.decode())
+            nbytes = int(req["nbytes"])
+            need = -(-max(1, nbytes) // ARENA_ALIGN) * ARENA_ALIGN
             try:
-                ptr = self.dev.alloc(int(req["nbytes"]))
-                self.dev.sync()
-                handle = self.dev.ipc_handle(ptr)
+                with self._lock:
+                    for arena in self._arenas:
+                        off = arena.take(need)
+                        if off is not None:
+                            break
+                    else:
+                        arena = _Arena(self.dev, max(need, ARENA_MIN))
+                        self._arenas.append(arena)
+                        off = arena.take(need)
+                    i = self._next
+                    self._next += 1
+                    self._dev[i] = (arena, off, need, nbytes, req.get("meta", {}))
             except Exception as exc:
                 send_frame(sock, D_ERR, f"device allocation failed: {exc}".encode())
                 return
-            i = self._new_id()
-            with self._lock:
-                self._dev[i] = (ptr, int(req["nbytes"]), handle, req.get("meta", {}))
-            send_frame(sock, D_OK, _U64.pack(i) + handle)
+            send_frame(sock, D_OK, _U64.pack(i) + arena.handle + _U64.pack(off) + _U64.pack(arena.serial))
         elif kind == D_DEV_OPEN:
             (i,) = _U64.unpack(body)
             with self._lock:
@@ -110,15 +160,18 @@ class GpuMemoryDaemon:
             if ent is None:
                 send_frame(sock, D_ERR, b"unknown allocation")
             else:
-                send_frame(sock, D_OK, ent[2] + json.dumps(ent[3]).encode())
+                arena, off = ent[0], ent[1]
+                send_frame(sock, D_OK, arena.handle + _U64.pack(off) + _U64.pack(arena.serial)
+                           + json.dumps(ent[4]).encode())
         elif kind == D_DEV_FREE:
             (i,) = _U64.unpack(body)
             with self._lock:
                 ent = self._dev.pop(i, None)
+                if ent is not None:
+                    ent[0].give(ent[1], ent[2])
             if ent is None:
                 send_frame(sock, D_ERR, b"unknown allocation")
                 return
-            self.dev.free(ent[0])
             send_frame(sock, D_OK, b"")
         else:
             send_frame(sock, D_ERR, b"bad request")
@@ -135,11 +188,12 @@ class GpuMemoryDaemon:
         self._server.shutdown()
         self._server.server_close()
         with self._lock:
-            for ptr, _n, _h, _m in self._dev.values():
+            for arena in self._arenas:
                 try:
-                    self.dev.free(ptr)
+                    self.dev.free(arena.ptr)
                 except Exception:
                     pass
+            self._arenas.clear()
             self._dev.clear()
         self.dev.close()
 
@@ -187,12 +241,16 @@ class DaemonClient:
         return struct.unpack("<QQ", self._call(D_STATS, b""))
 
     def dev_alloc(self, nbytes: int, meta: dict) -> tuple:
+        """-> (allocation id, arena IPC handle, offset in the arena, arena serial)."""
         reply = self._call(D_DEV_ALLOC, json.dumps({"nbytes": int(nbytes), "meta": meta}).encode())
-        return _U64.unpack_from(reply, 0)[0], reply[8:72]
+        return (_U64.unpack_from(reply, 0)[0], reply[8:72], _U64.unpack_from(reply, 72)[0],
+                _U64.unpack_from(reply, 80)[0])
 
     def dev_open(self, alloc_id: int) -> tuple:
+        """-> (arena IPC handle, offset, arena serial, meta)."""
         reply = self._call(D_DEV_OPEN, _U64.pack(alloc_id))
-        return reply[:64], json.loads(reply[64:].decode())
+        return (reply[:64], _U64.unpack_from(reply, 64)[0], _U64.unpack_from(reply, 72)[0],
+                json.loads(reply[80:].decode()))
 
     def dev_free(self, alloc_id: int) -> None:
         self._call(D_DEV_FREE, _U64.pack(alloc_id))

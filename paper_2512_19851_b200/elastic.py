@@ -123,8 +123,9 @@ def checkpoint_tiles(job, client: DaemonClient, owner: int) -> tuple:
     records = []
     if store is None:
         return records, {}
-    # allocate every blob first, then one batch of D2D copies and ONE sync
-    pending = []
+    # allocate every blob, one batch of D2D copies, ONE sync; each daemon
+    # arena is mapped once
+    arenas: dict = {}
     for coords in sorted(store.tiles):
         tile = store.tiles[coords]
         for a in sorted(store.arrays):
@@ -134,16 +135,17 @@ def checkpoint_tiles(job, client: DaemonClient, owner: int) -> tuple:
             header = blob_header(a, coords, ext, depth, tile.local_epoch[a])
             payload = int(np.prod(ext)) * buf.elem
             meta = {"header": header.hex(), "dtype": buf.dtype}
-            alloc_id, handle = client.dev_alloc(payload, meta)
-            dst = dev.ipc_open(handle)
-            dev.copy_box(_interior_box(buf, dst, True), buf.elem, COMPUTE)
-            pending.append(dst)
+            alloc_id, handle, off, serial = client.dev_alloc(payload, meta)
+            base = arenas.get(serial)
+            if base is None:
+                base = arenas[serial] = dev.ipc_open(handle)
+            dev.copy_box(_interior_box(buf, base + off, True), buf.elem, COMPUTE)
             records.append({"array": a, "tile": list(coords), "owner": owner,
                             "daemon": client.address, "alloc_id": alloc_id,
                             "nbytes": len(header) + payload})
     dev.sync()
-    for dst in pending:
-        dev.ipc_close(dst)
+    for base in arenas.values():
+        dev.ipc_close(base)
     arrays_meta = {}
     for a, info in store.arrays.items():
         depth = next((list(t.depths[a]) for t in store.tiles.values()), None)
@@ -202,7 +204,8 @@ def restore_tiles(job, manifest: dict) -> dict:
         # sequence aligned (tiles, if any, carry the same values in their blobs)
         store.set_epochs(a, int(meta.get("local_epoch", 0)), int(meta.get("local_epoch", 0)))
     clients: dict = {}
-    opened = []  # (client, alloc id, mapped address): all copies in flight, ONE sync
+    opened = []   # (client, alloc id): all copies in flight, ONE sync
+    arenas: dict = {}  # (daemon, arena serial) -> mapped base, each mapped once
     try:
         for rec in manifest["allocations"]:
             if rec["owner"] != job.rank:
@@ -210,7 +213,7 @@ def restore_tiles(job, manifest: dict) -> dict:
             cl = clients.get(rec["daemon"])
             if cl is None:
                 cl = clients[rec["daemon"]] = DaemonClient(rec["daemon"])
-            handle, meta = cl.dev_open(rec["alloc_id"])
+            handle, off, serial, meta = cl.dev_open(rec["alloc_id"])
             header = bytes.fromhex(meta["header"])
             a, coords, ext, depth, epoch, _hs = parse_blob_header(header)
             payload = int(np.prod(ext)) * (8 if int(meta.get("dtype", 0)) == 0 else 4)
@@ -218,16 +221,19 @@ def restore_tiles(job, manifest: dict) -> dict:
                 raise ValueError(f"allocation {rec['alloc_id']} size mismatch")
             tile = store.tiles.setdefault(tuple(coords), GpuTile(tuple(coords)))
             buf = TileBuffer(dev, ext, depth, int(meta.get("dtype", 0)))
-            src = dev.ipc_open(handle)
-            opened.append((cl, rec["alloc_id"], src))
-            dev.copy_box(_interior_box(buf, src, False), buf.elem, COMPUTE)
+            base = arenas.get((rec["daemon"], serial))
+            if base is None:
+                base = arenas[(rec["daemon"], serial)] = dev.ipc_open(handle)
+            opened.append((cl, rec["alloc_id"]))
+            dev.copy_box(_interior_box(buf, base + off, False), buf.elem, COMPUTE)
             tile.buffers[a] = buf
             tile.depths[a] = tuple(depth)
             tile.local_epoch[a] = epoch
             tile.ghost_epoch[a] = epoch
         dev.sync()
-        for cl, alloc_id, src in opened:
-            dev.ipc_close(src)
+        for base in arenas.values():
+            dev.ipc_close(base)
+        for cl, alloc_id in opened:
             cl.dev_free(alloc_id)
     finally:
         for cl in clients.values():
