@@ -72,8 +72,9 @@ class IpcPeerTransport(LocalPeerTransport):
         self.readers: dict = {}
         self.pull_launches = 0
         self.peer_events: dict = {}
-        self.peer_maps: dict = {}      # (owner, coords, array) -> (layout TileBuffer, addr, handle)
-        self.peer_tables: dict = {}    # (owner, coords, array) -> (handle, ext, depth, dtype)
+        self.peer_maps: dict = {}      # (owner, coords, array) -> (layout TileBuffer, addr, identity)
+        self.peer_tables: dict = {}    # (owner, coords, array) -> buffer_table entry
+        self.arena_maps: dict = {}     # (owner, arena serial) -> mapped base
         self.peer_event_handles: dict = {}
         self.spin_s = 0.0
         self.peer_version = 0
@@ -90,10 +91,15 @@ class IpcPeerTransport(LocalPeerTransport):
         self.peer_event_handles = {o: h for o, h in table.items() if o != self.w}
 
     def buffer_table(self) -> dict:
+        """(coords, array) -> (arena serial, arena IPC handle, offset, extents,
+        depth, dtype, buffer serial): buffers live in the worker's arenas
+        (pool.py), so a peer maps each arena once."""
         out = {}
+        pool = self.dev.pool
         for coords, tile in self.store.tiles.items():
             for array, buf in tile.buffers.items():
-                out[(tuple(coords), array)] = (self.dev.ipc_handle(buf.ptr), buf.ext[3 - buf.rank:],
+                serial, handle, off = pool.locate(buf.ptr)
+                out[(tuple(coords), array)] = (serial, handle, off, buf.ext[3 - buf.rank:],
                                                buf.depth[3 - buf.rank:], buf.dtype, buf.serial)
         return out
 
@@ -109,14 +115,10 @@ class IpcPeerTransport(LocalPeerTransport):
                 continue
             for (coords, array), entry in table.items():
                 wanted[(owner, tuple(coords), array)] = entry
-        for key, (layout, addr, handle) in list(self.peer_maps.items()):
+        for key, (_layout, _addr, ident) in list(self.peer_maps.items()):
             ent = wanted.get(key)
-            if ent is None or (ent[0], ent[4]) != handle:
-                try:
-                    self.dev.ipc_close(addr)
-                except Exception:
-                    pass
-                del self.peer_maps[key]
+            if ent is None or (ent[0], ent[2], ent[6]) != ident:
+                del self.peer_maps[key]  # the arena mapping itself stays (arenas live with the job)
         self.peer_tables = wanted
 
     def map_neighbours(self) -> int:
@@ -146,23 +148,31 @@ class IpcPeerTransport(LocalPeerTransport):
         return len(self.peer_maps) - before
 
     def close_peer_buffers(self) -> None:
-        for _layout, addr, _h in self.peer_maps.values():
-            try:
-                self.dev.ipc_close(addr)
-            except Exception:
-                pass
+        """Forget the per-buffer views (a realloc or migration republishes
+        the tables); the peers' arena mappings are kept until close()."""
         self.peer_maps.clear()
         self.peer_tables = {}
+
+    def close_arenas(self) -> None:
+        for base in self.arena_maps.values():
+            try:
+                self.dev.ipc_close(base)
+            except Exception:
+                pass
+        self.arena_maps.clear()
 
     # -- protocol hooks ----------------------------------------------------------
     def peer_buffer(self, owner: int, coords, array: int):
         key = (owner, tuple(coords), array)
         hit = self.peer_maps.get(key)
         if hit is None:
-            handle, ext, depth, dtype, serial = self.peer_tables[key]
-            addr = self.dev.ipc_open(handle)
+            aserial, handle, off, ext, depth, dtype, serial = self.peer_tables[key]
+            base = self.arena_maps.get((owner, aserial))
+            if base is None:
+                base = self.arena_maps[(owner, aserial)] = self.dev.ipc_open(handle)
+            addr = base + off
             layout = TileBuffer(self.dev, ext, depth, dtype, ptr=addr)
-            hit = self.peer_maps[key] = (layout, addr, (handle, serial))
+            hit = self.peer_maps[key] = (layout, addr, (aserial, off, serial))
         return hit[0], hit[1]
 
     def peer_event(self, owner: int, kind: str, slot: int):
@@ -207,6 +217,7 @@ class IpcPeerTransport(LocalPeerTransport):
 
     def close(self) -> None:
         self.close_peer_buffers()
+        self.close_arenas()
         for evs in self.peer_events.values():
             for lst in evs.values():
                 for e in lst:
@@ -239,6 +250,9 @@ class IpcGpuJob:
         self.rank, self.world, self.odf = rank, world, odf
         self.timeout_s = timeout_s
         self.dev = dev if dev is not None else Device(device)  # a worker may pre-create it
+        from .pool import DevicePool
+
+        self.dev.pool = DevicePool(self.dev)  # tile buffers in exported arenas, mapped once per peer
         self.devs = [self.dev]
         self.skeleton = skeleton
         self.decomp = decomp
@@ -394,6 +408,9 @@ class IpcGpuJob:
             pass
         if self.store is not None:
             self.store.release()
+        if getattr(self.dev, "pool", None) is not None:
+            self.dev.pool.release()
+            self.dev.pool = None
         if self._stage is not None:
             self._stage.close()
         if self.counters is not None:

@@ -28,6 +28,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from .pool import device_alloc, device_free
 from ._lib import EstBox
 from .device import COMPUTE, Device, PinnedBuffer
 from .errors import IndivisibleShape, InvalidShape, OffsetExceedsTileWidth
@@ -136,7 +137,7 @@ class TileBuffer:
         self.nz = self.ext[0] + 2 * dz
         self.nbytes = self.pz * self.nz * self.elem
         self.owned = ptr is None
-        self.ptr = dev.alloc(self.nbytes) if ptr is None else ptr
+        self.ptr = device_alloc(dev, self.nbytes) if ptr is None else ptr
         self.serial = next(TileBuffer._serials)  # identifies this allocation in peer tables
 
     @staticmethod
@@ -167,7 +168,7 @@ class TileBuffer:
 
     def free(self) -> None:
         if self.ptr and self.owned:
-            self.dev.free(self.ptr)
+            device_free(self.dev, self.ptr)
         self.ptr = 0
 
 
