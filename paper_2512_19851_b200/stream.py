@@ -34,6 +34,7 @@ from .codegen import CTYPE, ELEM, NodeSig, StmtSig, _emit_expr, slot_radius
 from .wire import DTYPE_F64
 
 MIN_ZCHUNK = 32
+STORE_HINT = os.environ.get("EST_STREAM_STHINT", "0") == "1"  # evict_first L2 policy on output stores
 MAX_RADIUS = 4
 SMEM_BUDGET = 220 * 1024
 SMEM_PER_SM = 228 * 1024
@@ -310,6 +311,9 @@ def source_ws2(sig: NodeSig, rank: int, cfg: StreamCfg) -> tuple:
     for s_ in sorted(regs):
         a(f"  T {', '.join(f'c{s_}_{r}_{k}' for r in range(RPT) for k in range(Z[s_]))};")
     a("  const long long opy = p.opy, opz = p.opz;")
+    if STORE_HINT:
+        a("  unsigned long long st_pol;  // outputs are not re-read by this launch: evict them first from L2")
+        a("  asm volatile(\"createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\" : \"=l\"(st_pol));")
     a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
     a("    const int bx = item % nbx, rest = item / nbx;")
     a("    const int by = rest % nby, bzc = rest / nby;")
@@ -375,7 +379,11 @@ def source_ws2(sig: NodeSig, rank: int, cfg: StreamCfg) -> tuple:
             a(f"        if (ok{r}) {{")
             for ln in lines:
                 a("          " + ln)
-            a(f"          orow[{r} * opy] = {res};")
+            if STORE_HINT:
+                a(f"          asm volatile(\"st.global.L2::cache_hint.{'f64' if elem == 8 else 'f32'} [%0], %1, %2;\""
+                  f" :: \"l\"(orow + {r} * opy), \"{'d' if elem == 8 else 'f'}\"({res}), \"l\"(st_pol) : \"memory\");")
+            else:
+                a(f"          orow[{r} * opy] = {res};")
             a("        }")
         a("        orow += opz;")
         a("        __syncwarp();")
