@@ -105,6 +105,15 @@ def postorder(root, out_start) -> tuple:
     return tuple(seq)
 
 
+def plan_key(instructions) -> tuple:
+    """Hashable identity of a postorder plan with constants as exact bit
+    patterns: as Python floats -0.0 == 0.0 (and NaN != NaN), so plans that
+    differ only in a signed zero would otherwise share cache entries."""
+    import struct
+
+    return tuple((i[0], struct.pack("<d", i[1])) if i[0] == OP_CONST else i for i in instructions)
+
+
 def compile_plan(node, ast_table) -> KernelPlan:
     plans = tuple(
         StatementPlan(postorder(ast_table[st.ast_id].root, st.output_slice.starts),

@@ -33,7 +33,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .analysis import OP_BINARY, OP_CONST, OP_LOAD, OP_UNARY
+from .analysis import OP_BINARY, OP_CONST, OP_LOAD, OP_UNARY, plan_key
 from .wire import DTYPE_F32, DTYPE_F64
 
 CTYPE = {DTYPE_F64: "double", DTYPE_F32: "float"}
@@ -257,7 +257,7 @@ def kernel_source_for(plan, rank: int, dtype: int, skeleton: str = "auto", small
     from . import stream
 
     cfg = stream.cfg_for(rank, small, dtype)
-    key = (tuple(p.instructions for p in plan.statements), rank, dtype, skeleton, cfg)
+    key = (tuple(plan_key(p.instructions) for p in plan.statements), rank, dtype, skeleton, cfg)
     hit = _SRC_CACHE.get(key)
     if hit is not None:
         return hit

@@ -28,7 +28,7 @@ import time
 from dataclasses import dataclass, field
 
 from . import codegen, resident, stream, temporal, wavefront
-from .analysis import KernelPlan, analyze_dag, compile_plan
+from .analysis import KernelPlan, analyze_dag, compile_plan, plan_key
 from .device import COMPUTE
 from .errors import MalformedDag
 
@@ -337,7 +337,7 @@ class GpuExecutor:
         ba, bb = tile.buffers[a], tile.buffers[b]
         if (ba.depth, ba.py, ba.pz, ba.xoff) != (bb.depth, bb.py, bb.pz, bb.xoff):
             return None
-        return (a, b, tuple(ps.output_slice_bounds), ps.instructions, ia.rank, ia.dtype)
+        return (a, b, tuple(ps.output_slice_bounds), plan_key(ps.instructions), ia.rank, ia.dtype)
 
     def _tb_candidate(self, plan):
         c = self._chain_candidate(plan)

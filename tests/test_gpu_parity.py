@@ -11,7 +11,7 @@ from golden_cases import case_names, get_case
 from oracle.oracle import (
     bits_equal, heat3d_reference, laplace_reference, reference_execute_dag, strict_execute_dag)
 from paper_2512_19851_b200.errors import MalformedDag, OffsetExceedsTileWidth
-from paper_2512_19851_b200.ir import Dag, DagNode, compute_edges, cst, ref
+from paper_2512_19851_b200.ir import Dag, DagNode, add, compute_edges, cst, mul, ref, sub
 from paper_2512_19851_b200.programs import (
     DagProgram, heat3d_program, laplace_program, wave2d_program)
 from paper_2512_19851_b200.session import GpuJob, run_program
@@ -263,5 +263,39 @@ def test_fused_cavity_split_into_stream_launches():
             assert bits_equal(job.fetch(aid), want[aid]), aid
         # kernel_launches keeps the reference definition (one per node per tile)
         assert sum(s.kernel_launches for b in stats for s in b) == sum(s.nodes_executed for b in stats for s in b)
+    finally:
+        job.close()
+
+
+@pytest.mark.parametrize("shape", [(40, 40, 40), (96, 80), (500,)])
+def test_ieee_specials_propagate(shape):
+    """inf / NaN / signed zero flow through the generated kernels exactly as
+    through numpy (executor.py:130, oracle.py:81): 1/0, 0/0, sqrt of a
+    negative, neg / abs of -0.0 and NaN, then a stencil over the result."""
+    from paper_2512_19851_b200.ir import div, neg, una
+    rank = len(shape)
+    prog = DagProgram()
+    a, b, c = (prog.create_array(shape) for _ in range(3))
+    q = [n // 4 for n in shape]
+    prog.assign(a, tuple((k, 2 * k) for k in q), cst(-2.0))
+    prog.assign(a, tuple((2 * k, 3 * k) for k in q), cst(-0.0))
+    full = tuple(slice(None) for _ in shape)
+    prog.assign(b, full, div(cst(1.0), ref(a, full)))                       # +-inf, -0.5
+    prog.assign(c, full, add(div(ref(a, full), ref(a, full)),              # NaN where a == 0
+                             una("abs", neg(una("sqrt", ref(a, full))))))   # NaN for negatives
+    inner = tuple(slice(1, -1) for _ in shape)
+    terms = None
+    for ax in range(rank):
+        for d in (-1, 1):
+            sl = tuple(slice(1 + (d if k == ax else 0), n - 1 + (d if k == ax else 0)) for k, n in enumerate(shape))
+            t = ref(b, sl)
+            terms = t if terms is None else add(terms, t)
+    prog.assign(a, inner, sub(mul(cst(0.5), terms), ref(c, inner)))
+    want = reference_execute_dag(prog.dag, prog.shapes)
+    assert np.isnan(want[a]).any() and np.isinf(want[b]).any()
+    job, _ = run_program(prog)
+    try:
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), aid
     finally:
         job.close()

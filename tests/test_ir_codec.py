@@ -118,3 +118,20 @@ def test_slice_and_command_codecs():
     assert decode_command(*encode_command(cmd)) == cmd
     cmd = Command(3, FETCH, array=2, slice=SliceSpec(((0, 4), (1, 2))))
     assert decode_command(*encode_command(cmd)) == cmd
+
+
+def test_kernel_cache_distinguishes_signed_zero():
+    """-0.0 == 0.0 as Python floats: generated kernels must still differ."""
+    from paper_2512_19851_b200.analysis import compile_plan, plan_key
+    from paper_2512_19851_b200.codegen import kernel_source_for
+    from paper_2512_19851_b200.ir import cst
+    from paper_2512_19851_b200.programs import DagProgram
+
+    prog = DagProgram()
+    a = prog.create_array((8, 8))
+    prog.assign(a, (slice(0, 4), slice(None)), cst(0.0))
+    prog.assign(a, (slice(0, 4), slice(None)), cst(-0.0))
+    p0, p1 = (compile_plan(n, prog.dag.ast_table) for n in prog.dag.nodes[-2:])
+    assert plan_key(p0.statements[0].instructions) != plan_key(p1.statements[0].instructions)
+    s0, s1 = kernel_source_for(p0, 2, 0)[0], kernel_source_for(p1, 2, 0)[0]
+    assert "0x8000000000000000" in s1 and "0x8000000000000000" not in s0
