@@ -109,9 +109,9 @@ class GpuExecutor:
         for node in dag.nodes:
             if len(node.statements) > 1 and node_hazard(node):
                 raise MalformedDag(f"node {node.node_id} has dependent statements")
-            dts = {self.store.arrays[a].dtype for s in node.statements for a in (s.output, *s.inputs)}
-            if len(dts) > 1:
-                raise MalformedDag(f"node {node.node_id} mixes element types")
+            for st in node.statements:
+                if len({self.store.arrays[a].dtype for a in (st.output, *st.inputs)}) > 1:
+                    raise MalformedDag(f"node {node.node_id}: a statement mixes element types")
         need: dict = {}
         for m in metas:
             for a, off in m.array_max_offset.items():
@@ -697,6 +697,16 @@ class GpuExecutor:
         return big + ([KernelPlan(plan.node_id, tuple(rest))] if rest else [])
 
     def _launch_node(self, node, plan, zsplit=None) -> None:
+        if len(plan.statements) > 1:
+            # a fused node's statements are independent; statements of other
+            # ranks / element types than the first go to their own launches
+            kinds = [(self.store.arrays[ps.output].rank, self.store.arrays[ps.output].dtype)
+                     for ps in plan.statements]
+            if len(set(kinds)) > 1:
+                for kind in sorted(set(kinds)):
+                    sub = tuple(ps for ps, k in zip(plan.statements, kinds) if k == kind)
+                    self._launch_node(node, KernelPlan(plan.node_id, sub), zsplit)
+                return
         boxes = self._boxes(plan)
         if not boxes:
             return

@@ -299,3 +299,29 @@ def test_ieee_specials_propagate(shape):
             assert bits_equal(job.fetch(aid), want[aid]), aid
     finally:
         job.close()
+
+
+def test_fused_node_mixing_ranks_and_dtypes():
+    """fuse() may merge independent statements on arrays of different rank or
+    element type into one node; each kind gets its own launch."""
+    from paper_2512_19851_b200.ir import fuse
+    prog = DagProgram()
+    a2, b2 = prog.create_array((16, 16)), prog.create_array((16, 16))
+    a3, b3 = prog.create_array((16, 16, 16)), prog.create_array((16, 16, 16))
+    f2, g2 = prog.create_array((16, 16), DTYPE_F32), prog.create_array((16, 16), DTYPE_F32)
+    prog.assign(a2, ((2, 9), (3, 12)), cst(1.5))
+    prog.assign(a3, ((2, 9), (3, 12), (1, 14)), cst(-2.25))
+    prog.assign(f2, ((4, 13), (1, 8)), cst(0.125))
+    i2, i3 = (slice(1, -1),) * 2, (slice(1, -1),) * 3
+    prog.assign(b2, i2, add(ref(a2, (slice(0, -2), slice(1, -1))), ref(a2, (slice(2, None), slice(1, -1)))))
+    prog.assign(b3, i3, add(ref(a3, (slice(0, -2), slice(1, -1), slice(1, -1))), ref(a3, i3)))
+    prog.assign(g2, i2, mul(cst(3.0), ref(f2, (slice(1, -1), slice(2, None)))))
+    fused = fuse(prog.dag)
+    assert any(len(n.statements) > 1 for n in fused.nodes)
+    want = reference_execute_dag(prog.dag, prog.shapes, prog.dtypes)
+    job, _ = run_program(prog, fused=True)
+    try:
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), aid
+    finally:
+        job.close()
