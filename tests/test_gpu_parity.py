@@ -325,3 +325,18 @@ def test_fused_node_mixing_ranks_and_dtypes():
             assert bits_equal(job.fetch(aid), want[aid]), aid
     finally:
         job.close()
+
+
+@pytest.mark.parametrize("workers,odf", [(2, 1), (1, 4), (2, 2), (4, 1)])
+def test_wave2d_fp32_multi_tile(workers, odf):
+    """fp32 halo strips (4-byte copies) between co-located tiles and peers."""
+    prog = DagProgram()
+    names = wave2d_program(prog, 128, 16, dtype=DTYPE_F32)
+    want = reference_execute_dag(prog.dag, prog.shapes, prog.dtypes)
+    job, _ = run_program(prog, workers=workers, odf=odf)
+    try:
+        for aid in prog.shapes:
+            got = job.fetch(aid)
+            assert got.dtype == np.float32 and bits_equal(got, want[aid]), (aid, workers, odf)
+    finally:
+        job.close()
