@@ -265,7 +265,9 @@ class IpcGpuJob:
         self.dtypes: dict = {}
         self._next = 0
         self._stage = None
-        self._decoded: dict = {}
+        from .wire import DagCache
+
+        self._decoded = DagCache()
         self.counters = None
         self._open_counters()
         if decomp is not None:
@@ -340,16 +342,7 @@ class IpcGpuJob:
         return aid
 
     def run_bytes(self, blob: bytes) -> list:
-        import hashlib
-
-        from .wire import decode_dag
-
-        key = hashlib.blake2b(blob, digest_size=16).digest()
-        dag = self._decoded.get(key)
-        if dag is None:
-            if len(self._decoded) > 64:
-                self._decoded.clear()
-            dag = self._decoded[key] = decode_dag(blob)
+        key, dag = self._decoded.get(blob)
         return self.run(dag, key)
 
     def run(self, dag, key: bytes | None = None) -> list:

@@ -40,7 +40,9 @@ class GpuJob:
         self.shapes: dict = {}
         self.dtypes: dict = {}
         self._stage = None
-        self._decoded: dict = {}
+        from .wire import DagCache
+
+        self._decoded = DagCache()
 
     def _build(self, shape) -> None:
         self.decomp = decompose(shape, self.workers, self.odf)
@@ -79,17 +81,7 @@ class GpuJob:
 
         Repeated batches skip decode and, on a single worker, replay a captured
         CUDA graph (executor.GpuExecutor.execute_batch `key`)."""
-        import hashlib
-
-        from .wire import decode_dag
-
-        key = hashlib.blake2b(blob, digest_size=16).digest()
-        dag = self._decoded.get(key)
-        if dag is None:
-            dag = decode_dag(blob)
-            if len(self._decoded) > 64:
-                self._decoded.clear()
-            self._decoded[key] = dag
+        key, dag = self._decoded.get(blob)
         return self.run(dag, key)
 
     def run(self, dag, key: bytes | None = None) -> list:
