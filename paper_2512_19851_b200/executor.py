@@ -86,6 +86,7 @@ class GpuExecutor:
         self.replays = 0
         self.temporal = temporal.ENABLED  # fuse ping-pong sweep chains (temporal.py)
         self.resident = resident.ENABLED  # whole L2-resident chains in one launch (resident.py)
+        self.resident_smem = resident.SMEM_ENABLED  # small rank-2 chains held in shared memory
         self.wave = wavefront.ENABLED     # sweep pairs forwarded through L2 in one launch (wavefront.py)
         self._wave_ctr = (0, 0)           # (device pointer, bytes) of the wave ticket/progress counters
         self._bar = 0                     # grid-barrier counter of the resident skeleton
@@ -285,6 +286,8 @@ class GpuExecutor:
                     self._launch_tb(node, plan, chain[1], key)
                 elif chain[0] == "res":
                     self._launch_resident(node, plan, chain[1], key)
+                elif chain[0] == "rsm":
+                    self._launch_resident_smem(node, plan, chain[1], key)
                 elif chain[0] == "wave":
                     self._launch_wave(node, plan, key)
             elif pending and set(pending) & set(meta.array_max_offset) and self.overlap_eligible(plan):
@@ -356,11 +359,11 @@ class GpuExecutor:
         the number of chains kept even so A ends in its own buffer. Only for
         one tile per job without transport (no exchange between sweeps);
         everything else runs node by node."""
-        if (not (self.temporal or self.resident or self.wave) or self.transport is not None
+        if (not (self.temporal or self.resident or self.resident_smem or self.wave) or self.transport is not None
                 or len(self.store.tiles) != 1 or self.store.decomp.n_tiles != 1
                 or self.skeleton not in ("auto", "tb")):
             return {}
-        ck = ((key, self.store.version, self.tb_cfg, self.temporal, self.resident, self.wave)
+        ck = ((key, self.store.version, self.tb_cfg, self.temporal, self.resident, self.resident_smem, self.wave)
               if key is not None else None)
         hit = self._tb_sched.get(ck) if ck is not None else None
         if hit is not None:
@@ -380,7 +383,12 @@ class GpuExecutor:
                    and cand[j][0] == cand[j - 1][1] and cand[j][1] == cand[j - 1][0]):
                 j += 1
             sig = codegen.stmt_sig(plans[i].statements[0], c[4])
-            if (self.resident and j - i >= 2 and resident.eligible(sig, c[5], c[4])
+            if (self.resident_smem and j - i >= 2 and resident.smem_eligible(sig, c[5], c[4])
+                    and self._rsm_geometry(c, sig) is not None):
+                sched[dag.nodes[i].node_id] = ("rsm", j - i)
+                for q in range(i + 1, j):
+                    sched[dag.nodes[q].node_id] = ("member",)
+            elif (self.resident and j - i >= 2 and resident.eligible(sig, c[5], c[4])
                     and resident.fits_l2(tile.buffers[c[0]])):
                 sched[dag.nodes[i].node_id] = ("res", j - i)
                 for q in range(i + 1, j):
@@ -486,6 +494,48 @@ class GpuExecutor:
         self._recording = [] if ck is not None else None
         try:
             self._launch(kern, grid, params, tag=("res", sweeps))
+        finally:
+            rec, self._recording = self._recording, None
+        if ck is not None and rec is not None:
+            self._launches[ck] = rec
+
+    def _rsm_geometry(self, c, sig):
+        (y0, y1), (x0, x1) = c[2]
+        return resident.smem_geometry(y1 - y0, x1 - x0, resident.slot_radius(sig)[0], c[5], self.dev.sm_count)
+
+    def _launch_resident_smem(self, node, plan, sweeps: int, key) -> None:
+        """One persistent launch running `sweeps` ping-pong sweeps out of
+        shared memory, KM sweeps per pair of grid barriers (resident.py)."""
+        ps = plan.statements[0]
+        a, b = ps.inputs[0], ps.output
+        tile = next(iter(self.store.tiles.values()))
+        ba, bb = tile.buffers[a], tile.buffers[b]
+        info = self.store.arrays[a]
+        if not self._bar:
+            self._bar = self.dev.alloc(256)
+        self.dev.memset_zero(self._bar, 4, COMPUTE)
+        ck = (key, node.node_id, self.store.version, "rsm") if key is not None else None
+        rec = self._launches.get(ck) if ck is not None else None
+        if rec is not None and not self.time_kernels:
+            for kern, grid, params in rec:
+                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
+            return
+        sig = codegen.stmt_sig(ps, 2)
+        c = self._chain_candidate(plan)
+        geo = self._rsm_geometry(c, sig)
+        src, name, block, smem = resident.smem_source(sig, info.dtype, geo)
+        kern = self.dev.kernel(src, name, block, smem)
+        dy, dx = ba.depth[1], ba.depth[2]
+        (y0, y1), (x0, x1) = ps.output_slice_bounds
+        org = ba.xoff * ba.elem
+        params = resident.smem_pack_params(ba.ptr + org, bb.ptr + org, self._bar, ba.py,
+                                           (y0 + dy, x0 + dx), (y1 + dy, x1 + dx), sweeps, geo)
+        grid = (geo.ntx * geo.nty, 1, 1)
+        if self.dev.occupancy(kern) < 1 or grid[0] > self.dev.sm_count:
+            raise RuntimeError("resident-smem chain kernel cannot be resident on this device")
+        self._recording = [] if ck is not None else None
+        try:
+            self._launch(kern, grid, params, tag=("rsm", sweeps))
         finally:
             rec, self._recording = self._recording, None
         if ck is not None and rec is not None:

@@ -29,6 +29,7 @@ def mode(request, monkeypatch):
     monkeypatch.setattr(temporal, "ENABLED", request.param.startswith("tb"))
     monkeypatch.setattr(resident, "ENABLED", request.param == "resident")
     monkeypatch.setattr(wavefront, "ENABLED", request.param == "wave")
+    monkeypatch.setattr(resident, "SMEM_ENABLED", False)  # tests/test_gpu_resident_smem.py
     if request.param == "tb-warp":
         monkeypatch.setattr(temporal, "DEFAULT", dataclasses.replace(temporal.DEFAULT, variant="warp"))
     return "tb" if request.param.startswith("tb") else request.param

@@ -15,7 +15,7 @@ from paper_2512_19851_b200.tiles import ArrayInfo, GpuTileStore, decompose
 from paper_2512_19851_b200.wire import DTYPE_F32, DTYPE_F64
 
 
-def _executor(shapes, workers=1, odf=1, temporal_on=True, resident_on=False):
+def _executor(shapes, workers=1, odf=1, temporal_on=True, resident_on=False, rsm_on=False):
     dev = FakeDevice()
     shape = next(iter(shapes.values()))
     decomp = decompose(shape, workers, odf)
@@ -27,6 +27,7 @@ def _executor(shapes, workers=1, odf=1, temporal_on=True, resident_on=False):
     ex = GpuExecutor(store, mgr)
     ex.temporal = temporal_on
     ex.resident = resident_on
+    ex.resident_smem = rsm_on
     ex.wave = False
     return ex, store, mgr, dev
 
@@ -254,3 +255,82 @@ def test_wave_ticket_order_is_deadlock_free(nxy, nzb):
         zb = i // nxy
         for b in range(max(zb - 1, 0), min(zb + 1, nzb - 1) + 1):
             assert all(pos[(1, b * nxy + k)] < pos[(2, i)] for k in range(nxy))
+
+
+# ---------------------------------------------------------------------------
+# resident-smem chains (resident.py): small rank-2 runs held in shared memory
+
+def _laplace(n, iters):
+    from paper_2512_19851_b200.programs import laplace_iteration_statements, laplace_program
+    setup, step = DagProgram(), DagProgram()
+    names = laplace_program(setup, n, 0)
+    for a in sorted(setup.shapes):
+        step.builder.declare_array(a, setup.shapes[a])
+    laplace_iteration_statements(step, names["u"], names["scratch"], iters)
+    return setup, step
+
+
+@pytest.mark.parametrize("iters", [2, 9, 100])
+def test_resident_smem_run_is_one_launch(iters):
+    setup, step = _laplace(64, iters)
+    ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, rsm_on=True)
+    ex.execute_batch(setup.dag)
+    dev.log.clear()
+    stats = ex.execute_batch(step.dag)
+    assert _names(dev) == ["est_resident_smem"]
+    assert stats.kernel_launches == iters and stats.nodes_executed == iters
+
+
+def test_resident_smem_bookkeeping_matches_node_by_node():
+    setup, step = _laplace(64, 9)
+    res = []
+    for on in (True, False):
+        ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, rsm_on=on)
+        ex.execute_batch(setup.dag)
+        st = [ex.execute_batch(step.dag, b"k") for _ in range(4)]
+        res.append(({a: (store.local_epoch(a), store.ghost_epoch(a)) for a in store.arrays},
+                    dict(mgr.rounds_started),
+                    [(s.nodes_executed, s.kernel_launches, s.rounds, s.net_messages) for s in st]))
+    assert res[0] == res[1]
+
+
+def test_resident_smem_scope():
+    """Rank 2 only, one tile, and only when one tile per SM fits shared memory."""
+    setup, step = _laplace(64, 6)
+    plans = [compile_plan(n, step.dag.ast_table) for n in step.dag.nodes]
+    ex, *_ = _executor(setup.shapes, temporal_on=False, rsm_on=True)
+    assert ex.temporal_schedule(step.dag, plans)[step.dag.nodes[0].node_id] == ("rsm", 6)
+    ex, *_ = _executor(setup.shapes, 1, 2, temporal_on=False, rsm_on=True)
+    assert ex.temporal_schedule(step.dag, plans) == {}
+    big, bstep = _laplace(4096, 2)   # 2 x 128 MiB: no one-tile-per-SM fit
+    bplans = [compile_plan(n, bstep.dag.ast_table) for n in bstep.dag.nodes]
+    ex, *_ = _executor(big.shapes, temporal_on=False, rsm_on=True)
+    assert ex.temporal_schedule(bstep.dag, bplans) == {}
+    h, hstep = _heat(4)              # rank 3 is not a resident-smem chain
+    hplans = [compile_plan(n, hstep.dag.ast_table) for n in hstep.dag.nodes]
+    ex, *_ = _executor(h.shapes, temporal_on=False, rsm_on=True)
+    assert ex.temporal_schedule(hstep.dag, hplans) == {}
+
+
+@pytest.mark.parametrize("ny,nx,rad,dtype", [(1022, 1022, (0, 1, 1), DTYPE_F64), (1022, 1022, (0, 1, 1), DTYPE_F32),
+                                             (60, 200, (0, 2, 2), DTYPE_F64), (1, 1000, (0, 1, 1), DTYPE_F64),
+                                             (1500, 1500, (0, 1, 1), DTYPE_F32)])
+def test_resident_smem_geometry_covers_s(ny, nx, rad, dtype):
+    from paper_2512_19851_b200 import resident
+    g = resident.smem_geometry(ny, nx, rad, dtype, 148)
+    assert g is not None
+    assert g.ntx * g.nty <= 148 and g.ntx * g.tx >= nx and g.nty * g.ty >= ny
+    assert (g.ntx - 1) * g.tx < nx and (g.nty - 1) * g.ty < ny
+    assert g.smem(rad, dtype) <= resident.SMEM_BUDGET
+
+
+def test_resident_smem_kernel_source():
+    from paper_2512_19851_b200 import resident
+    setup, step = _laplace(32, 1)
+    plan = compile_plan(step.dag.nodes[-1], step.dag.ast_table)
+    sig = codegen.stmt_sig(plan.statements[0], 2)
+    assert resident.smem_eligible(sig, DTYPE_F64, 2) and not resident.smem_eligible(sig, DTYPE_F64, 3)
+    geo = resident.smem_geometry(30, 30, (0, 1, 1), DTYPE_F64, 148)
+    src, name, block, smem = resident.smem_source(sig, DTYPE_F64, geo)
+    assert name == "est_resident_smem" and block == (geo.threads, 1, 1) and smem == geo.smem((0, 1, 1), DTYPE_F64)
+    assert src.count("grid_sync(bar,") == 3 and "__dadd_rn" in src and "__stcg" in src
