@@ -83,16 +83,21 @@ def bytes_per_launch(w, tag) -> int:
     """Algorithmic HBM bytes of one launch of kernel kind `tag` = (kind, sweeps).
 
     A plain node kernel is one sweep (bytes_per_iter). A temporal chain of K
-    sweeps (temporal.py) reads the input array once and writes each of the two
-    arrays once: elem * (N_in + 2 * N_out)."""
+    sweeps (temporal.py) reads the input array once and writes A once; B is
+    written only by the last chain of a run (temporal.SKIP_MID_B), so per
+    launch: elem * (N_in + N_out) + elem * N_out / chains per run."""
     kind, sweeps = tag
     if kind in ("res", "rsm"):  # resident chains: every sweep counts as a full pass (data in L2 / smem)
         return bytes_per_iter(w) * sweeps
     if kind != "tb":
         return bytes_per_iter(w)
+    from paper_2512_19851_b200 import temporal
     n = w["n"]
     m = n - 2
-    return 8 * ((m ** 3 + 6 * m ** 2) + 2 * m ** 3)
+    chains = w["iters_per_step"] // sweeps
+    chains -= chains % 2
+    b_writes = 8 * m ** 3 if not temporal.SKIP_MID_B else 8 * m ** 3 / max(1, chains)
+    return int(8 * ((m ** 3 + 6 * m ** 2) + m ** 3) + b_writes)
 
 
 def load_peaks() -> tuple:

@@ -65,6 +65,13 @@ def node_hazard(node) -> bool:
     return False
 
 
+def _volume(bounds) -> int:
+    v = 1
+    for lo, hi in bounds:
+        v *= max(0, hi - lo)
+    return v
+
+
 class GpuExecutor:
     def __init__(self, store, exchanges, skeleton: str = "auto"):
         self.store = store
@@ -283,7 +290,7 @@ class GpuExecutor:
                 # kernel; members only keep the per-node bookkeeping (a single
                 # tile without transport has no device work between sweeps)
                 if chain[0] == "lead":
-                    self._launch_tb(node, plan, chain[1], key)
+                    self._launch_tb(node, plan, chain[1], key, chain[2])
                 elif chain[0] == "res":
                     self._launch_resident(node, plan, chain[1], key)
                 elif chain[0] == "rsm":
@@ -350,7 +357,7 @@ class GpuExecutor:
         return c if temporal.eligible(sig, c[5], self.tb_cfg) else None
 
     def temporal_schedule(self, dag, plans, key=None) -> dict:
-        """node id -> ("res", sweeps) | ("lead", chain index in its run) | ("member",).
+        """node id -> ("res", sweeps) | ("lead", chain index in its run, last in run) | ("member",).
 
         Runs of consecutive candidate nodes that ping-pong A -> B -> A with the
         same statement and output slice: if both arrays fit in L2 the whole
@@ -397,12 +404,13 @@ class GpuExecutor:
                 for ch in range((j - i) // 2):
                     sched[dag.nodes[i + 2 * ch].node_id] = ("wave", ch)
                     sched[dag.nodes[i + 2 * ch + 1].node_id] = ("member",)
-            elif self.temporal and c[4] == 3 and temporal.eligible(sig, c[5], self.tb_cfg):
+            elif (self.temporal and c[4] == 3 and temporal.eligible(sig, c[5], self.tb_cfg)
+                  and _volume(c[2]) >= temporal.MIN_POINTS):
                 m = (j - i) // K
                 m -= m % 2
                 for ch in range(m):
                     lead = i + ch * K
-                    sched[dag.nodes[lead].node_id] = ("lead", ch)
+                    sched[dag.nodes[lead].node_id] = ("lead", ch, ch == m - 1)
                     for q in range(1, K):
                         sched[dag.nodes[lead + q].node_id] = ("member",)
             i = j
@@ -557,7 +565,7 @@ class GpuExecutor:
             tw.free()
         self._scratch.clear()
 
-    def _launch_tb(self, node, plan, ch: int, key) -> None:
+    def _launch_tb(self, node, plan, ch: int, key, last: bool = True) -> None:
         ps = plan.statements[0]
         a, b = ps.inputs[0], ps.output
         tile = next(iter(self.store.tiles.values()))
@@ -583,7 +591,7 @@ class GpuExecutor:
         tm = self._tmap(src_buf, (lay["w0"], lay["h0"], 1), self.tb_cfg.l2promo)
         org = home.xoff * home.elem
         params = temporal.pack_params(tm, src_buf.ptr + org, bbuf.ptr + org, dst_buf.ptr + org,
-                                      home, s_lo, s_hi, geo)
+                                      home, s_lo, s_hi, geo, write_b=last or not temporal.SKIP_MID_B)
         self._recording = [] if ck is not None else None
         try:
             self._launch(kern, (geo["blocks"], 1, 1), params, tag=("tb", self.tb_cfg.k))

@@ -42,13 +42,14 @@ from .stream import _PTX_HELPERS
 MAX_RADIUS = 2
 SMEM_BUDGET = 200 * 1024
 SMEM_PER_SM = 228 * 1024
+SKIP_MID_B = os.environ.get("EST_TB_SKIPB", "1") == "1"
 
 
 @dataclass(frozen=True)
 class TbCfg:
     k: int = 2              # sweeps per launch (even)
-    bx: int = 64            # output columns per item
-    by: int = 16            # output rows per item
+    bx: int = 48            # output columns per item
+    by: int = 32            # output rows per item
     rpt: int = 2            # rows of the step-1 region per compute thread
     prefetch: int = 2       # input planes in flight beyond the z window
     zchunk: int = 128       # planes per item
@@ -73,7 +74,11 @@ def _env_cfg() -> TbCfg:
 
 
 DEFAULT = _env_cfg()
-ENABLED = os.environ.get("EST_TB", "0") == "1"
+ENABLED = os.environ.get("EST_TB", "1") == "1"
+# measured crossover (profiles/r1s2_tb_skipb.md): at 1022^3 outputs the chain
+# beats two single sweeps by 18 %, at 510^3 it is 1.5-4 % slower (too few
+# items per SM to hide each item's pipeline fill)
+MIN_POINTS = int(os.environ.get("EST_TB_MIN_POINTS", 1 << 28))
 
 
 def _round(v: int, m: int) -> int:
@@ -177,7 +182,7 @@ def source_block(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
     a("struct __align__(64) Params { Tmap tm;")
     a("  unsigned long long src, bhome, adst;  // padded-box origins: A now, B (in place), A next")
     a("  long long py, pz;")
-    a("  int npz, npy, npx, xoff, sz0, sz1, sy0, sy1, sx0, sx1, nbx, nby, zc, nzc; };")
+    a("  int npz, npy, npx, xoff, sz0, sz1, sy0, sy1, sx0, sx1, nbx, nby, zc, nzc, wb; };")
     L.append(_PTX_HELPERS)
     a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
     a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
@@ -340,7 +345,7 @@ def source_warp(st: StmtSig, dtype: int, cfg: TbCfg) -> tuple:
     a("struct __align__(64) Params { Tmap tm;")
     a("  unsigned long long src, bhome, adst;  // padded-box origins: A now, B (in place), A next")
     a("  long long py, pz;")
-    a("  int npz, npy, npx, xoff, sz0, sz1, sy0, sy1, sx0, sx1, nbx, nby, zc, nzc; };")
+    a("  int npz, npy, npx, xoff, sz0, sz1, sy0, sy1, sx0, sx1, nbx, nby, zc, nzc, wb; };")
     L.append(_PTX_HELPERS)
     a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
     a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
@@ -439,7 +444,7 @@ def source_warp(st: StmtSig, dtype: int, cfg: TbCfg) -> tuple:
                 a(f"            {ln}")
             a(f"            v = {res};")
             if 0 <= r < R:
-                a(f"            if (own) bmem[zo1 + {r} * py] = v;")
+                a(f"            if (own && p.wb) bmem[zo1 + {r} * py] = v;")
             a(f"          }} else {{")
             a(f"            v = (zp1 && rP{rr}) ? bmem[zo1 + {r} * py] : ({T})0;  // outside S: stored value")
             a("          }")
@@ -565,7 +570,7 @@ def emit_fast_loop(a, st: StmtSig, dtype: int, lay: dict) -> None:
                     a(f"{ind}        Wr[so{r}] = {res};")
                     a(f"{ind}        {col(j, r, 2 * rz)} = {res};")
                     if j == K - 1:
-                        a(f"{ind}        if (inT{K}_{r}) *bp{r} = {res};")
+                        a(f"{ind}        if (p.wb && inT{K}_{r}) *bp{r} = {res};")
                 a(f"{ind}      }}")
             a(f"{ind}    }}")
             if not final:
@@ -639,7 +644,7 @@ def emit_step_b(a, st: StmtSig, dtype: int, lay: dict, j: int) -> None:
         if final:
             a(f"{ind}    adst[zoff + go{r}] = v;")
         elif j == K - 1:
-            a(f"{ind}    if (inT{K}_{r}) bmem[zoff + go{r}] = v;")
+            a(f"{ind}    if (p.wb && inT{K}_{r}) bmem[zoff + go{r}] = v;")
         a(f"{ind}  }} else {{")
         a(f"{ind}    v = {'(T)0' if final else f'h{j}_{r}'};")
         a(f"{ind}  }}")
@@ -665,15 +670,18 @@ def item_geometry(s_lo, s_hi, sm_count: int, lay: dict) -> dict:
     return {"nbx": nbx, "nby": nby, "zc": zc, "nzc": nzc, "blocks": blocks}
 
 
-def pack_params(tmap: bytes, src: int, bhome: int, adst: int, buf, s_lo, s_hi, geo: dict) -> bytes:
+def pack_params(tmap: bytes, src: int, bhome: int, adst: int, buf, s_lo, s_hi, geo: dict,
+                write_b: bool = True) -> bytes:
     """Params block (layout mirrored in `source`). Pointers are padded-box
-    origins (buffer base + xoff elements)."""
+    origins (buffer base + xoff elements). `write_b` False skips B's stores:
+    inside a run only the last chain's B survives (the next chain overwrites
+    B before anything reads it), so earlier chains move 16 B per K LUP."""
     assert len(tmap) == 128
     npz, npy, npx = buf.nz, buf.pz // buf.py, buf.ext[2] + 2 * buf.depth[2]
     out = bytearray(tmap)
     out += struct.pack("<QQQqq", src, bhome, adst, buf.py, buf.pz)
-    out += struct.pack("<14i", npz, npy, npx, buf.xoff, s_lo[0], s_hi[0], s_lo[1], s_hi[1],
-                       s_lo[2], s_hi[2], geo["nbx"], geo["nby"], geo["zc"], geo["nzc"])
+    out += struct.pack("<15i", npz, npy, npx, buf.xoff, s_lo[0], s_hi[0], s_lo[1], s_hi[1],
+                       s_lo[2], s_hi[2], geo["nbx"], geo["nby"], geo["zc"], geo["nzc"], int(write_b))
     return bytes(out) + b"\0" * ((-len(out)) % 64)
 
 

@@ -51,6 +51,7 @@ class FakeDevice:
         self.launches = 0
         self.sm_count = 148
         self.log: list = []
+        self.params: list = []
         self.copies: list = []
         self._next = 1 << 40
         self.allocated: dict = {}
@@ -99,6 +100,7 @@ class FakeDevice:
     def launch(self, k, grid, params, stream=0, pdl=True):
         self.launches += 1
         self.log.append(("launch", grid[0], getattr(k, "name", "")))
+        self.params.append(params)
 
     def tmap_3d(self, base, elem, dims, strides, box, l2_promotion=3):
         return base.to_bytes(8, "little").ljust(128, b"\0")

@@ -30,6 +30,7 @@ def mode(request, monkeypatch):
     monkeypatch.setattr(resident, "ENABLED", request.param == "resident")
     monkeypatch.setattr(wavefront, "ENABLED", request.param == "wave")
     monkeypatch.setattr(resident, "SMEM_ENABLED", False)  # tests/test_gpu_resident_smem.py
+    monkeypatch.setattr(temporal, "MIN_POINTS", 0)  # chains at test sizes
     if request.param == "tb-warp":
         monkeypatch.setattr(temporal, "DEFAULT", dataclasses.replace(temporal.DEFAULT, variant="warp"))
     return "tb" if request.param.startswith("tb") else request.param

@@ -15,6 +15,11 @@ from paper_2512_19851_b200.tiles import ArrayInfo, GpuTileStore, decompose
 from paper_2512_19851_b200.wire import DTYPE_F32, DTYPE_F64
 
 
+@pytest.fixture(autouse=True)
+def _small_grids_chain(monkeypatch):
+    monkeypatch.setattr(temporal, "MIN_POINTS", 0)  # chains at test sizes (default: large grids only)
+
+
 def _executor(shapes, workers=1, odf=1, temporal_on=True, resident_on=False, rsm_on=False):
     dev = FakeDevice()
     shape = next(iter(shapes.values()))
@@ -334,3 +339,30 @@ def test_resident_smem_kernel_source():
     src, name, block, smem = resident.smem_source(sig, DTYPE_F64, geo)
     assert name == "est_resident_smem" and block == (geo.threads, 1, 1) and smem == geo.smem((0, 1, 1), DTYPE_F64)
     assert src.count("grid_sync(bar,") == 3 and "__dadd_rn" in src and "__stcg" in src
+
+
+def test_tb_only_for_large_grids(monkeypatch):
+    monkeypatch.setattr(temporal, "MIN_POINTS", 1 << 28)
+    setup, step = _heat(4)
+    plans = [compile_plan(n, step.dag.ast_table) for n in step.dag.nodes]
+    ex, *_ = _executor(setup.shapes)
+    assert ex.temporal_schedule(step.dag, plans) == {}
+    monkeypatch.setattr(temporal, "MIN_POINTS", 14 ** 3)
+    ex, *_ = _executor(setup.shapes)
+    assert [v[0] for v in ex.temporal_schedule(step.dag, plans).values()] == ["lead", "member", "lead", "member"]
+
+
+def test_b_written_only_by_the_last_chain_of_a_run():
+    """B's stores are skipped in every chain but the run's last (the next
+    chain rewrites B before anything reads it); the Params flag sits after
+    the tensor map, five 64-bit fields and fourteen ints."""
+    import struct
+    setup, step = _heat(8)
+    ex, store, mgr, dev = _executor(setup.shapes)
+    ex.execute_batch(setup.dag)
+    dev.params.clear()
+    dev.log.clear()
+    ex.execute_batch(step.dag)
+    tb = [p for e, p in zip(dev.log, dev.params) if e[2] == "est_tb"]
+    assert len(tb) == 4
+    assert [struct.unpack_from("<i", p, 128 + 40 + 14 * 4)[0] for p in tb] == [0, 0, 0, 1]
