@@ -83,6 +83,10 @@ def standard_sources() -> list:
                     rs = _ss(plan.statements[0], rank)
                     if resident.eligible(rs, dt, rank):
                         srcs.add(resident.source(rs, dt, rank)[0])
+                    if resident.smem_eligible(rs, dt, rank):  # C1: 1022^2 outputs on 148 SMs
+                        g = resident.smem_geometry(1022, 1022, resident.slot_radius(rs)[0], dt, 148)
+                        if g is not None:
+                            srcs.add(resident.smem_source(rs, dt, g)[0])
                 if rank == 3 and len(plan.statements) == 1:
                     from . import temporal
                     from .codegen import stmt_sig
