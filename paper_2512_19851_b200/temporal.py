@@ -132,7 +132,9 @@ def eligible(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> bool:
     cfg = cfg or DEFAULT
     if warp_eligible(st, dtype, cfg):
         return True
-    if cfg.k < 2 or cfg.k % 2 or st.arity != 1 or dtype not in ELEM or not z_star(st):
+    # only K = 2 is validated: a K = 4 launch faulted (illegal address) on
+    # B200 (scripts/gpu_tb_k4.sh), so deeper chains are not scheduled
+    if cfg.k != 2 or st.arity != 1 or dtype not in ELEM or not z_star(st):
         return False
     rad = slot_radius(st).get(0)
     if rad is None or max(rad) > MAX_RADIUS or rad[0] < 1:
