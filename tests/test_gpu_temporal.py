@@ -238,3 +238,23 @@ def test_resident_2d_laplace_and_wave_sizes(mode):
         assert bits_equal(job.fetch(names["u"]), want[names["u"]])
     finally:
         job.close()
+
+
+def test_default_chain_at_full_scheduling_size(mode, monkeypatch):
+    """The default path (tb from 2^28 output points) at a size where it is
+    actually scheduled: 648^3 (646^3 = 269.6 M outputs), 4 iterations = 2
+    chains, seeded fills; every array bit-identical to the strict oracle."""
+    if mode != "tb":
+        pytest.skip("the size threshold only gates tb")
+    from paper_2512_19851_b200 import temporal
+    monkeypatch.setattr(temporal, "MIN_POINTS", 1 << 28)
+    prog = DagProgram()
+    heat3d_program(prog, 648, 4, seed_fills=12)
+    want = strict_execute_dag(prog.dag, prog.shapes)
+    job, _ = run_program(prog)
+    try:
+        assert _ran(job, mode)
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), aid
+    finally:
+        job.close()
