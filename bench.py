@@ -172,8 +172,18 @@ class ClockSampler:
 # --------------------------------------------------------------------------
 # CPU baseline / reference arm (oracle port, test infrastructure)
 
+def host_threads() -> int:
+    """Every core this process may run on (torchrun exports OMP_NUM_THREADS=1
+    to its ranks, so OpenMP's own default is not used)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_sample(w, iters: int = 2, planes: int = 34, threads: int = 0) -> dict:
     """Strict-order C oracle on a bounded sample of the workload, all host cores."""
+    threads = threads or host_threads()
     from oracle.oracle import _lib as olib, strict_eval_statement
     from paper_2512_19851_b200.analysis import compile_plan
     from paper_2512_19851_b200.programs import DagProgram, heat3d_program, laplace_program
