@@ -171,3 +171,46 @@ def test_graph_replay_batches():
         assert stats[1][0].gpu_launches == 1
         for aid in setup.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), aid
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_chains(seed):
+    """Random ping-pong chains: shape, output box, offsets (radius <= 3 per
+    axis, any sign, cross terms), constants, dtype and sweep count."""
+    rng = random.Random(9000 + seed)
+    ny, nx = rng.randrange(12, 320), rng.randrange(12, 320)
+    r = (rng.randrange(0, 4), rng.randrange(0, 4))
+    lo = (rng.randrange(r[0], r[0] + 4), rng.randrange(r[1], r[1] + 4))
+    hi = (ny - rng.randrange(r[0], r[0] + 4), nx - rng.randrange(r[1], r[1] + 4))
+    if hi[0] <= lo[0] or hi[1] <= lo[1]:
+        pytest.skip("empty box")
+    box = (lo, hi)
+    dtype = rng.choice((DTYPE_F32, DTYPE_F64))
+    prog = DagProgram()
+    u1, u2 = prog.create_array((ny, nx), dtype), prog.create_array((ny, nx), dtype)
+    _fills(prog, (u1, u2), (ny, nx), rng, 8)
+    offs = {(0, 0)} | {(rng.randrange(-r[0], r[0] + 1), rng.randrange(-r[1], r[1] + 1)) for _ in range(5)}
+    offs = sorted(offs)
+    consts = [round(rng.uniform(-1, 1), 4) for _ in offs]
+    signs = [rng.random() < 0.7 for _ in offs]
+
+    def tree(u):
+        s = None
+        for (dy, dx), c, plus in zip(offs, consts, signs):
+            t = mul(cst(c), ref(u, ((lo[0] + dy, hi[0] + dy), (lo[1] + dx, hi[1] + dx))))
+            s = t if s is None else (add(s, t) if plus else sub(s, t))
+        return s
+
+    a, b = u1, u2
+    sl = (slice(lo[0], hi[0]), slice(lo[1], hi[1]))
+    for _ in range(rng.randrange(2, 26)):
+        prog.assign(b, sl, tree(a))
+        a, b = b, a
+    want = strict_execute_dag(prog.dag, prog.shapes, prog.dtypes)
+    job, _ = run_program(prog)
+    try:
+        assert _ran(job)
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), (seed, aid)
+    finally:
+        job.close()
