@@ -258,3 +258,53 @@ def test_default_chain_at_full_scheduling_size(mode, monkeypatch):
             assert bits_equal(job.fetch(aid), want[aid]), aid
     finally:
         job.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_z_star_chains(seed, mode):
+    """Random 3-D ping-pong chains the tb skeleton accepts (in-plane offsets
+    of radius <= 2 in y/x, pure z offsets of radius 1-2, any signs), random
+    boxes, constants, dtypes and even sweep counts."""
+    if mode != "tb":
+        pytest.skip("tb-specific shapes")
+    import random as _r
+    rng = _r.Random(7700 + seed)
+    n = (rng.randrange(12, 60), rng.randrange(12, 90), rng.randrange(12, 90))
+    rz, ry, rx = rng.randrange(1, 3), rng.randrange(0, 3), rng.randrange(0, 3)
+    lo = (rz + rng.randrange(0, 3), ry + rng.randrange(0, 3), rx + rng.randrange(0, 3))
+    hi = (n[0] - rz - rng.randrange(0, 3), n[1] - ry - rng.randrange(0, 3), n[2] - rx - rng.randrange(0, 3))
+    from paper_2512_19851_b200.wire import DTYPE_F64
+    dtype = rng.choice((DTYPE_F32, DTYPE_F64))
+    prog = DagProgram()
+    u1, u2 = prog.create_array(n, dtype), prog.create_array(n, dtype)
+    for u in (u1, u2):
+        for _ in range(6):
+            a = [rng.randrange(0, e) for e in n]
+            b = [rng.randrange(x + 1, e + 1) for x, e in zip(a, n)]
+            prog.assign(u, tuple(slice(x, y) for x, y in zip(a, b)), cst(round(rng.uniform(-4, 4), 3)))
+    offs = {(0, 0, 0), (rz, 0, 0), (-rng.randrange(1, rz + 1), 0, 0)}
+    offs |= {(0, rng.randrange(-ry, ry + 1), rng.randrange(-rx, rx + 1)) for _ in range(4)}
+    offs = sorted(offs)
+    consts = [round(rng.uniform(-1, 1), 4) for _ in offs]
+    signs = [rng.random() < 0.7 for _ in offs]
+
+    def tree(u):
+        s = None
+        for (dz, dy, dx), c, plus in zip(offs, consts, signs):
+            t = mul(cst(c), ref(u, tuple((l + d, h + d) for l, h, d in zip(lo, hi, (dz, dy, dx)))))
+            s = t if s is None else (add(s, t) if plus else sub(s, t))
+        return s
+
+    a, b = u1, u2
+    box = tuple(slice(l, h) for l, h in zip(lo, hi))
+    for _ in range(2 * rng.randrange(2, 7)):  # >= 4 sweeps: chains come in pairs
+        prog.assign(b, box, tree(a))
+        a, b = b, a
+    want = strict_execute_dag(prog.dag, prog.shapes, prog.dtypes)
+    job, _ = run_program(prog)
+    try:
+        assert _ran(job, mode)
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), (seed, aid)
+    finally:
+        job.close()
