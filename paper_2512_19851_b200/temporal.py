@@ -52,7 +52,7 @@ class TbCfg:
     by: int = 32            # output rows per item
     rpt: int = 2            # rows of the step-1 region per compute thread
     prefetch: int = 2       # input planes in flight beyond the z window
-    zchunk: int = 128       # planes per item
+    zchunk: int = 192       # planes per item (C4: 5 full chunks + 62; 1-2 % over 128, profiles/r1s2_tb_skipb.md)
     l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
     persistent: bool = False
     minb: int = 0           # __launch_bounds__ min blocks per SM (0: from smem/threads, >= 48 regs)
