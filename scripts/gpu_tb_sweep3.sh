@@ -10,11 +10,8 @@ import json; d=json.loads(open('gpurun_out/tbs.json').read().strip().splitlines(
 print('$label', round(d['value'],1), d['roofline']['kernel'], round(d['roofline']['kernel_ms'],3), d['clocks']['sm_mhz'])" || tail -3 gpurun_out/tbs.err
 }
 run "default"
-run "zc171" EST_TB_ZCHUNK=171
-run "zc192" EST_TB_ZCHUNK=192
-run "zc205" EST_TB_ZCHUNK=205
-run "zc256" EST_TB_ZCHUNK=256
-run "zc146" EST_TB_ZCHUNK=146
+run "pf3" EST_TB_PREFETCH=3
+run "pf4" EST_TB_PREFETCH=4
+run "pf6" EST_TB_PREFETCH=6
+run "pf1" EST_TB_PREFETCH=1
 run "default again"
-run "zc171 again" EST_TB_ZCHUNK=171
-run "zc192 again" EST_TB_ZCHUNK=192
