@@ -347,6 +347,38 @@ class GpuTileStore:
         self.dev.stream_sync(COMPUTE)
         stage.close()
 
+    # -- checkpoint blobs (grid.py:236-277) ------------------------------------
+    def checkpoint_blob(self, coords, array: int) -> bytes:
+        """checkpoint_blob (grid.py:239-250): header + the tile interior, little
+        endian, ghost frame dropped; D2H through pinned staging. Byte-identical
+        to the reference for float64 (tests/golden/blobs.json)."""
+        info = self.arrays[array]
+        tile = self.tiles[tuple(coords)]
+        origin = self.decomp.tile_origin(info.shape, tuple(coords))
+        ext = self.decomp.tile_extents(info.shape)
+        pieces = self.gather_slice_pieces(array, tuple((o, o + e) for o, e in zip(origin, ext)))
+        (piece, block), = [pb for pb in pieces if tuple(a for a, _ in pb[0]) == tuple(origin)]
+        header = blob_header(array, tuple(coords), ext, tile.depths[array], tile.local_epoch[array])
+        return header + np.ascontiguousarray(block).astype(block.dtype.newbyteorder("<"), copy=False).tobytes()
+
+    def adopt_blob(self, blob: bytes) -> tuple:
+        """adopt_blob (grid.py:264-277): install a checkpointed interior into
+        the owned tile (ghost frame grown to the blob's depth if needed and
+        zeroed), epochs from the blob. -> (array, coords, epoch)."""
+        array, coords, ext, depth, epoch, hs = parse_blob_header(blob)
+        info = self.arrays[array]
+        if tuple(ext) != tuple(self.decomp.tile_extents(info.shape)):
+            raise InvalidShape(f"blob extent {ext} does not match array {array}'s tiles")
+        self.ensure_ghost_capacity(array, depth)
+        buf = self.tiles[coords].buffers[array]
+        self.dev.memset_zero(buf.ptr, buf.nbytes, COMPUTE)
+        data = np.frombuffer(blob, dtype=np.dtype(NP_DTYPE[info.dtype]).newbyteorder("<"),
+                             offset=hs).reshape(ext)
+        self.upload_interior(coords, array, data)
+        tile = self.tiles[coords]
+        tile.local_epoch[array] = tile.ghost_epoch[array] = epoch
+        return array, coords, epoch
+
     def release(self) -> None:
         for tile in self.tiles.values():
             for buf in tile.buffers.values():
