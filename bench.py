@@ -223,11 +223,55 @@ def cpu_sample(w, iters: int = 2, planes: int = 34, threads: int = 0) -> dict:
             "seconds": dt_s}
 
 
+def reference_runtime_sample(w, workers: int) -> dict | None:
+    """C1 through the reference's OWN runtime and public API (BASELINE.md §3:
+    Launcher + BatchingSession, flush 100, as pkg/src/elastencil/bench.py
+    does), installed in baseline/_ref; None if it is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if w["kind"] != "laplace" or not os.path.isdir(os.path.join(ref, "elastencil")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    os.environ["PYTHONPATH"] = ref + os.pathsep + os.environ.get("PYTHONPATH", "")  # spawned workers
+    from elastencil.bench import bench as ref_bench  # the reference, unmodified
+
+    r = ref_bench("laplace", w["n"], w["iters_per_step"], workers=workers)
+    lups = (w["n"] - 2) ** 2 * w["iters_per_step"]
+    return {"value": lups / r["wall_s"] / 1e9, "seconds": r["wall_s"], "oracle_ok": r["oracle_ok"]}
+
+
 def run_reference_arm(args, w):
-    """The reference's CPU path (oracle port) on the host cores, rank 0 only."""
+    """The reference's CPU path on the host cores, rank 0 only: for C1 the
+    reference runtime itself (baseline/_ref), otherwise the oracle port."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if w["kind"] == "laplace":
+        workers = 1
+        while workers * 2 <= min(8, host_threads()):
+            workers *= 2
+        if reference_runtime_sample(w, workers) is not None:  # warm-up (spawn, imports)
+            vals = []
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                vals.append(reference_runtime_sample(w, workers)["value"])
+            wall = time.perf_counter() - t0
+            value = statistics.median(vals)
+            sample = (f"each step: the reference runtime (baseline/_ref elastencil, Launcher + "
+                      f"BatchingSession flush 100, {workers} worker processes) running Laplace "
+                      f"{w['n']}^2 x {w['iters_per_step']} end to end, verified against laplace_reference")
+            line = {
+                "impl": "reference", "metric": METRIC, "value": value, "unit": "GLUP/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": 1,
+                "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic",
+                "config": {"workload": w["label"], "grid": [w["n"]] * 2},
+                "cpu_baseline": {"value": value, "unit": "GLUP/s", "cores": workers, "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": value, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            }
+            print(json.dumps(line), flush=True)
+            return
     planes = 34 if w["kind"] == "heat3d" else 8
     for _ in range(args.warmup):
         cpu_sample(w, iters=1, planes=planes)
