@@ -79,6 +79,8 @@ ENABLED = os.environ.get("EST_TB", "1") == "1"
 # beats two single sweeps by 18 %, at 510^3 it is 1.5-4 % slower (too few
 # items per SM to hide each item's pipeline fill)
 MIN_POINTS = int(os.environ.get("EST_TB_MIN_POINTS", 1 << 28))
+# chain depths that passed the GPU parity suite (EST_TB_VALIDATED_K widens it for experiments)
+VALIDATED_K = tuple(int(k) for k in os.environ.get("EST_TB_VALIDATED_K", "2").split(","))
 
 
 def _round(v: int, m: int) -> int:
@@ -132,9 +134,10 @@ def eligible(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> bool:
     cfg = cfg or DEFAULT
     if warp_eligible(st, dtype, cfg):
         return True
-    # only K = 2 is validated: a K = 4 launch faulted (illegal address) on
-    # B200 (scripts/gpu_tb_k4.sh), so deeper chains are not scheduled
-    if cfg.k != 2 or st.arity != 1 or dtype not in ELEM or not z_star(st):
+    # K = 4 chains are bit-exact since the padded-z guard of the fast path
+    # (scripts/debug_tb_k4.py) but 1.5-1.7x slower than K = 2 on C4
+    # (profiles/r1s2_tb_skipb.md), so only K = 2 is scheduled by default
+    if cfg.k not in VALIDATED_K or st.arity != 1 or dtype not in ELEM or not z_star(st):
         return False
     rad = slot_radius(st).get(0)
     if rad is None or max(rad) > MAX_RADIUS or rad[0] < 1:
@@ -576,10 +579,14 @@ def emit_fast_loop(a, st: StmtSig, dtype: int, lay: dict) -> None:
                 a(f"{ind}      }}")
             a(f"{ind}    }}")
             if not final:
-                a(f"{ind}    else {{  // plane outside S: the array's stored value")
+                a(f"{ind}    else {{  // plane outside S: the array's stored value (0 beyond the padded box,")
+                a(f"{ind}           // which deeper chains reach at the first and last planes)")
+                a(f"{ind}      const int zq = zs - {(K - j) * rz} + t - {2 * j * rz};")
+                a(f"{ind}      const bool zp = zq >= 0 && zq < p.npz;")
                 for r in range(RPT):
                     inT = "act" if j == 1 else f"inT{j}_{r}"
-                    a(f"{ind}      if ({inT}) {{ const T v = {home}[zo + go{r}]; Wr[so{r}] = v; {col(j, r, 2 * rz)} = v; }}")
+                    a(f"{ind}      if ({inT}) {{ const T v = zp ? {home}[zo + go{r}] : (T)0; Wr[so{r}] = v;"
+                      f" {col(j, r, 2 * rz)} = v; }}")
                 a(f"{ind}    }}")
             for r in range(RPT):
                 if final:
