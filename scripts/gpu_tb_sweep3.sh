@@ -10,8 +10,8 @@ import json; d=json.loads(open('gpurun_out/tbs.json').read().strip().splitlines(
 print('$label', round(d['value'],1), d['roofline']['kernel'], round(d['roofline']['kernel_ms'],3), d['clocks']['sm_mhz'])" || tail -3 gpurun_out/tbs.err
 }
 run "default"
-run "pf3" EST_TB_PREFETCH=3
-run "pf4" EST_TB_PREFETCH=4
-run "pf6" EST_TB_PREFETCH=6
-run "pf1" EST_TB_PREFETCH=1
+run "48x16 minb2" EST_TB_BX=48 EST_TB_BY=16 EST_TB_MINB=2
+run "48x16" EST_TB_BX=48 EST_TB_BY=16
+run "32x16 minb3" EST_TB_BX=32 EST_TB_BY=16 EST_TB_MINB=3
+run "32x22 minb2" EST_TB_BX=32 EST_TB_BY=22 EST_TB_MINB=2
 run "default again"
