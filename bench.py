@@ -535,7 +535,14 @@ def main():
                      **({"note": "the chain keeps the grid in shared memory (resident.py resident-smem); "
                                  "achieved counts each sweep's algorithmic bytes as if streamed from HBM, "
                                  "so frac compares against the single-sweep HBM bound it replaces"}
-                        if dom[0] == "rsm" else {})},
+                        if dom[0] == "rsm" else {}),
+                     **({"note": "achieved counts the bytes a 2-sweep chain must move (A read once, A written "
+                                 "once, B once per run); sweep_equivalent counts what the same sweeps move as "
+                                 "single sweeps, i.e. the HBM bandwidth a non-fused kernel would need for this rate",
+                         "sweep_equivalent": {
+                             "achieved": bytes_per_iter(w) // max(1, world) * sweeps / (mean_k / 1e3) / 1e9,
+                             "frac": bytes_per_iter(w) // max(1, world) * sweeps / (mean_k / 1e3) / 1e9 / peak}}
+                        if dom[0] == "tb" else {})},
         "e2e": {"value": e2e_val, "unit": "GLUP/s",
                 "h2d_bytes_per_step": len(blob), "d2h_bytes_per_step": d2h,
                 "note": ("per step: the W_BATCH payload (DAG bytes) from host memory -> decode/analysis cache -> "
