@@ -68,6 +68,8 @@ def migrate_tiles(job, plan: dict) -> dict:
     known = [e for e in job._all_gather(epochs) if e is not None]
     epochs = known[0] if known else {}
     job.barrier()
+    t_agree = time.perf_counter()
+    t_alloc = 0.0
     incoming = sorted(c for c, (old, new) in plan.items() if new == job.rank and old != job.rank)
     outgoing = sorted(c for c, (old, new) in plan.items() if old == job.rank and new != job.rank)
     depths = job.executor.depths
@@ -79,7 +81,9 @@ def migrate_tiles(job, plan: dict) -> dict:
             info = store.arrays[a]
             ext = store.decomp.tile_extents(info.shape)
             depth = depths.get(a, (0,) * info.rank)
+            ta = time.perf_counter()
             buf = TileBuffer(dev, ext, depth, info.dtype)
+            t_alloc += time.perf_counter() - ta
             src_layout, src_addr = job.transport.peer_buffer(old, coords, a)
             # src_layout describes the peer buffer; its ptr is the mapped address
             src = src_layout.interior_addr((0,) * info.rank)
@@ -110,6 +114,7 @@ def migrate_tiles(job, plan: dict) -> dict:
     job.exchange_buffers()
     return {"tiles_in": len(incoming), "tiles_out": len(outgoing), "bytes_in": nbytes,
             "pull_ms": round((t1 - t0) * 1e3, 1), "barrier_free_ms": round((t2 - t1) * 1e3, 1),
+            "agree_ms": round((t_agree - t0) * 1e3, 1), "alloc_ms": round(t_alloc * 1e3, 1),
             "peer_maps_ms": round((time.perf_counter() - t2) * 1e3, 1)}
 
 

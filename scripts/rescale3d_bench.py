@@ -76,11 +76,11 @@ def rank_body(rank, world, n, iters, planes):
     out["glups"]["initial_8"] = phase()
     ms, st = redistribute(world // 2)
     out["redistribute_ms"]["8->4"], out["moved_bytes"]["8->4"] = ms, st["bytes_in"]
-    out["stages"]["8->4"] = {k: st[k] for k in ("pull_ms", "barrier_free_ms", "peer_maps_ms")}
+    out["stages"]["8->4"] = {k: st[k] for k in ("pull_ms", "barrier_free_ms", "peer_maps_ms", "agree_ms", "alloc_ms")}
     out["glups"]["shrunk_4"] = phase()
     ms, st = redistribute(world)
     out["redistribute_ms"]["4->8"], out["moved_bytes"]["4->8"] = ms, st["bytes_in"]
-    out["stages"]["4->8"] = {k: st[k] for k in ("pull_ms", "barrier_free_ms", "peer_maps_ms")}
+    out["stages"]["4->8"] = {k: st[k] for k in ("pull_ms", "barrier_free_ms", "peer_maps_ms", "agree_ms", "alloc_ms")}
     out["glups"]["restored_8"] = phase()
     sample = {p: job.fetch(u, ((p, p + 1), (0, n), (0, n))) for p in planes}
     job.close()
