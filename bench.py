@@ -502,7 +502,7 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            pkey = args.workload + ("_tb%d" % sweeps if dom[0] == "tb" else "")
+            pkey = args.workload + {"tb": "_tb%d" % sweeps, "rsm": "_rsm%d" % sweeps}.get(dom[0], "")
             traffic = json.load(open(prof)).get(pkey, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
