@@ -89,6 +89,11 @@ int est_kernel_set_smem(uint64_t fn, int bytes);
  * or reads - every generated skeleton does; replaces the per-node launch gap
  * of executor.py:320-324's statement-at-a-time loop) */
 #define EST_LAUNCH_PDL 1
+/* EST_LAUNCH_COOPERATIVE: the driver guarantees every CTA of the grid is
+ * co-resident (or the launch fails with an error instead of the grid-barrier
+ * kernels spinning into their bounded trap); the kernel must take ONE
+ * parameter (the params block). */
+#define EST_LAUNCH_COOPERATIVE 2
 int est_launch_ex(est_ctx *ctx, uint64_t fn, const uint32_t grid[3], const uint32_t block[3],
                   uint32_t smem, const void *params, uint32_t params_size, int stream, int flags);
 /* resident CTAs per SM for a launch shape (persistent grids with grid-wide

@@ -81,8 +81,6 @@ def standard_sources() -> list:
                     from . import resident
                     from .codegen import stmt_sig as _ss
                     rs = _ss(plan.statements[0], rank)
-                    if resident.eligible(rs, dt, rank):
-                        srcs.add(resident.source(rs, dt, rank)[0])
                     if resident.smem_eligible(rs, dt, rank):  # C1: 1022^2 outputs on 148 SMs
                         g = resident.smem_geometry(1022, 1022, resident.slot_radius(rs)[0], dt, 148)
                         if g is not None:
@@ -92,7 +90,10 @@ def standard_sources() -> list:
                     from .codegen import stmt_sig
                     sig = stmt_sig(plan.statements[0], 3)
                     if temporal.eligible(sig, dt):
-                        srcs.add(temporal.source(sig, dt)[0])
+                        from .tiles import TileBuffer
+                        for n in (1024, 512):  # the C4 / C2 bench layouts (depth 1)
+                            xoff, py, pz = TileBuffer.pitches((n, n, n), (1, 1, 1), dt)
+                            srcs.add(temporal.source(sig, dt, py=py, pz=pz, xoff=xoff)[0])
     return sorted(srcs)
 
 

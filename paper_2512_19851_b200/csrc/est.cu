@@ -497,16 +497,25 @@ extern "C" int est_launch(est_ctx *c, uint64_t fn, const uint32_t grid[3], const
 
 extern "C" int est_launch_ex(est_ctx *c, uint64_t fn, const uint32_t grid[3], const uint32_t block[3],
                              uint32_t smem, const void *params, uint32_t params_size, int s, int flags) {
-    if (!(flags & EST_LAUNCH_PDL)) return est_launch(c, fn, grid, block, smem, params, params_size, s);
+    if (!(flags & (EST_LAUNCH_PDL | EST_LAUNCH_COOPERATIVE)))
+        return est_launch(c, fn, grid, block, smem, params, params_size, s);
     if ((uint64_t)grid[0] * grid[1] * grid[2] == 0) return 0;
     if (driver()) return 1;
     CUDA_TRY(cudaSetDevice(c->device));
     size_t sz = params_size;
     void *extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void *>(params),
                      CU_LAUNCH_PARAM_BUFFER_SIZE, &sz, CU_LAUNCH_PARAM_END};
-    CUlaunchAttribute attr[1];
-    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
-    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    void *kparams[] = {const_cast<void *>(params)};  // cooperative: the single params-block argument
+    CUlaunchAttribute attr[2];
+    unsigned n = 0;
+    if (flags & EST_LAUNCH_PDL) {
+        attr[n].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+        attr[n++].value.programmaticStreamSerializationAllowed = 1;
+    }
+    if (flags & EST_LAUNCH_COOPERATIVE) {
+        attr[n].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+        attr[n++].value.cooperative = 1;
+    }
     CUlaunchConfig cfg = {};
     cfg.gridDimX = grid[0];
     cfg.gridDimY = grid[1];
@@ -517,8 +526,11 @@ extern "C" int est_launch_ex(est_ctx *c, uint64_t fn, const uint32_t grid[3], co
     cfg.sharedMemBytes = smem;
     cfg.hStream = (CUstream)pick(c, s);
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CU_TRY(g_drv.launchKernelEx(&cfg, (CUfunction)(uintptr_t)fn, nullptr, extra));
+    cfg.numAttrs = n;
+    if (flags & EST_LAUNCH_COOPERATIVE)
+        CU_TRY(g_drv.launchKernelEx(&cfg, (CUfunction)(uintptr_t)fn, kparams, nullptr));
+    else
+        CU_TRY(g_drv.launchKernelEx(&cfg, (CUfunction)(uintptr_t)fn, nullptr, extra));
     return 0;
 }
 

@@ -200,14 +200,17 @@ class Device:
                                             C.byref(n)))
         return n.value
 
-    def launch(self, k: Kernel, grid, params: bytes, stream: int = COMPUTE, pdl: bool = True) -> None:
+    def launch(self, k: Kernel, grid, params: bytes, stream: int = COMPUTE, pdl: bool = True,
+               cooperative: bool = False) -> None:
         """`pdl`: the caller allows programmatic dependent launch here (no
         cross-stream / cross-process event waits interleaved with the
-        predecessor kernel)."""
+        predecessor kernel). `cooperative`: grid-barrier kernels; the driver
+        guarantees co-residency or fails the launch."""
         g = (C.c_uint32 * 3)(*grid)
         b = (C.c_uint32 * 3)(*k.block)
-        if pdl and k.pdl:
-            check(self.lib.est_launch_ex(self.ctx, k.fn, g, b, k.smem, params, len(params), stream, 1))
+        flags = (1 if (pdl and k.pdl) else 0) | (2 if cooperative else 0)
+        if flags:
+            check(self.lib.est_launch_ex(self.ctx, k.fn, g, b, k.smem, params, len(params), stream, flags))
         else:
             check(self.lib.est_launch(self.ctx, k.fn, g, b, k.smem, params, len(params), stream))
         self.launches += 1

@@ -27,10 +27,11 @@ import os
 import time
 from dataclasses import dataclass, field
 
-from . import codegen, resident, stream, temporal, wavefront
+from . import codegen, resident, stream, temporal
 from .analysis import KernelPlan, analyze_dag, compile_plan, plan_key
 from .device import COMPUTE
 from .errors import MalformedDag
+from .ir import validate_dag
 
 
 @dataclass
@@ -92,11 +93,8 @@ class GpuExecutor:
         self._replay: dict = {}
         self.replays = 0
         self.temporal = temporal.ENABLED  # fuse ping-pong sweep chains (temporal.py)
-        self.resident = resident.ENABLED  # whole L2-resident chains in one launch (resident.py)
         self.resident_smem = resident.SMEM_ENABLED  # small rank-2 chains held in shared memory
-        self.wave = wavefront.ENABLED     # sweep pairs forwarded through L2 in one launch (wavefront.py)
-        self._wave_ctr = (0, 0)           # (device pointer, bytes) of the wave ticket/progress counters
-        self._bar = 0                     # grid-barrier counter of the resident skeleton
+        self._bar = 0                     # grid-barrier counter of the resident-smem skeleton
         self.tb_cfg = temporal.DEFAULT
         self._scratch: dict = {}     # array -> twin TileBuffer for temporal chains
         self._tb_sched: dict = {}
@@ -108,6 +106,11 @@ class GpuExecutor:
         if cached is not None:
             metas, plans = cached
         else:
+            # the in-process API (GpuJob.run / run_bytes) has no coordinator in
+            # front of it (coordinator.py:417 validates there): re-validate every
+            # DAG not seen before, so e.g. a statement reading its own output
+            # raises SelfDependency instead of racing inside a fused kernel
+            validate_dag(dag, shapes)
             metas = analyze_dag(dag, shapes)
             plans = [compile_plan(n, dag.ast_table) for n in dag.nodes]
             if key is not None:
@@ -202,9 +205,27 @@ class GpuExecutor:
         if self._state_sig()[0] != sig[1][0]:
             return stats  # buffers were reallocated: not a steady-state batch
         if not capture:
-            self._replay[sig] = {"effects": self._effects(before, after), "stats": stats}
+            self._remember(sig, {"effects": self._effects(before, after), "stats": stats})
         stats.wall_ms = (time.perf_counter() - t0) * 1e3
         return stats
+
+    REPLAY_CAP = 64
+
+    def _remember(self, sig, ent: dict) -> None:
+        """Bounded replay cache: entries of an older buffer layout (store
+        version) can never match again and are dropped with their graphs; past
+        REPLAY_CAP the oldest entry goes."""
+        version = sig[1][0]
+        for old in [k for k in self._replay if k[1][0] != version]:
+            self._forget(old)
+        while len(self._replay) >= self.REPLAY_CAP:
+            self._forget(next(iter(self._replay)))
+        self._replay[sig] = ent
+
+    def _forget(self, sig) -> None:
+        ent = self._replay.pop(sig)
+        if ent.get("graph") is not None:
+            ent["graph"].close()
 
     def _epoch_snapshot(self) -> dict:
         st, ex = self.store, self.exchanges
@@ -256,9 +277,6 @@ class GpuExecutor:
         if self._bar:
             self.dev.free(self._bar)
             self._bar = 0
-        if self._wave_ctr[0]:
-            self.dev.free(self._wave_ctr[0])
-            self._wave_ctr = (0, 0)
 
     # -- execution (executor.py:258-348) ------------------------------------
     def _execute(self, dag, key: bytes | None = None) -> BatchStats:
@@ -291,12 +309,8 @@ class GpuExecutor:
                 # tile without transport has no device work between sweeps)
                 if chain[0] == "lead":
                     self._launch_tb(node, plan, chain[1], key, chain[2])
-                elif chain[0] == "res":
-                    self._launch_resident(node, plan, chain[1], key)
                 elif chain[0] == "rsm":
                     self._launch_resident_smem(node, plan, chain[1], key)
-                elif chain[0] == "wave":
-                    self._launch_wave(node, plan, key)
             elif pending and set(pending) & set(meta.array_max_offset) and self.overlap_eligible(plan):
                 # halo/compute overlap: planes that read no ghost cells go first,
                 # the deferred peer pull runs on the copy lane meanwhile, the
@@ -340,6 +354,8 @@ class GpuExecutor:
         if len(ps.inputs) != 1:
             return None
         a, b = ps.inputs[0], ps.output
+        if a == b:  # never chained: the kernels read A while writing B (validate_dag rejects it anyway)
+            return None
         ia, ib = self.store.arrays.get(a), self.store.arrays.get(b)
         if ia is None or ib is None or ia.rank not in (2, 3) or ia.shape != ib.shape or ia.dtype != ib.dtype:
             return None
@@ -357,20 +373,20 @@ class GpuExecutor:
         return c if temporal.eligible(sig, c[5], self.tb_cfg) else None
 
     def temporal_schedule(self, dag, plans, key=None) -> dict:
-        """node id -> ("res", sweeps) | ("lead", chain index in its run, last in run) | ("member",).
+        """node id -> ("rsm", sweeps) | ("lead", chain index in its run, last in run) | ("member",).
 
         Runs of consecutive candidate nodes that ping-pong A -> B -> A with the
-        same statement and output slice: if both arrays fit in L2 the whole
-        run is one resident launch (resident.py); otherwise, with temporal
+        same statement and output slice: a small rank-2 run is one
+        shared-memory-resident launch (resident.py); otherwise, with temporal
         chains enabled, the run is cut into chains of K nodes (temporal.py),
         the number of chains kept even so A ends in its own buffer. Only for
         one tile per job without transport (no exchange between sweeps);
         everything else runs node by node."""
-        if (not (self.temporal or self.resident or self.resident_smem or self.wave) or self.transport is not None
+        if (not (self.temporal or self.resident_smem) or self.transport is not None
                 or len(self.store.tiles) != 1 or self.store.decomp.n_tiles != 1
                 or self.skeleton not in ("auto", "tb")):
             return {}
-        ck = ((key, self.store.version, self.tb_cfg, self.temporal, self.resident, self.resident_smem, self.wave)
+        ck = ((key, self.store.version, self.tb_cfg, self.temporal, self.resident_smem)
               if key is not None else None)
         hit = self._tb_sched.get(ck) if ck is not None else None
         if hit is not None:
@@ -395,15 +411,6 @@ class GpuExecutor:
                 sched[dag.nodes[i].node_id] = ("rsm", j - i)
                 for q in range(i + 1, j):
                     sched[dag.nodes[q].node_id] = ("member",)
-            elif (self.resident and j - i >= 2 and resident.eligible(sig, c[5], c[4])
-                    and resident.fits_l2(tile.buffers[c[0]])):
-                sched[dag.nodes[i].node_id] = ("res", j - i)
-                for q in range(i + 1, j):
-                    sched[dag.nodes[q].node_id] = ("member",)
-            elif self.wave and c[4] == 3 and wavefront.eligible(sig, c[5]):
-                for ch in range((j - i) // 2):
-                    sched[dag.nodes[i + 2 * ch].node_id] = ("wave", ch)
-                    sched[dag.nodes[i + 2 * ch + 1].node_id] = ("member",)
             elif (self.temporal and c[4] == 3 and temporal.eligible(sig, c[5], self.tb_cfg)
                   and _volume(c[2]) >= temporal.MIN_POINTS):
                 m = (j - i) // K
@@ -419,93 +426,6 @@ class GpuExecutor:
                 self._tb_sched.clear()
             self._tb_sched[ck] = sched
         return sched
-
-    def _launch_wave(self, node, plan, key) -> None:
-        """Two sweeps (this node and the next) in one launch, in place (wavefront.py)."""
-        ps = plan.statements[0]
-        a, b = ps.inputs[0], ps.output
-        tile = next(iter(self.store.tiles.values()))
-        ba, bb = tile.buffers[a], tile.buffers[b]
-        info = self.store.arrays[a]
-        cfg = wavefront.DEFAULT
-        d = ba.depth
-        s_lo = tuple(lo + dd for (lo, _), dd in zip(ps.output_slice_bounds, d))
-        s_hi = tuple(hi + dd for (_, hi), dd in zip(ps.output_slice_bounds, d))
-        geo = wavefront.geometry(s_lo, s_hi, cfg)
-        need = 4 * (1 + geo["nzb"])
-        ptr, size = self._wave_ctr
-        if size < need:
-            if ptr:
-                self.dev.free(ptr)
-            size = max(need, 4096)
-            ptr = self.dev.alloc(size)
-            self._wave_ctr = (ptr, size)
-        self.dev.memset_zero(ptr, need, COMPUTE)
-        ck = (key, node.node_id, self.store.version, "wave") if key is not None else None
-        rec = self._launches.get(ck) if ck is not None else None
-        if rec is not None and not self.time_kernels:
-            for kern, grid, params in rec:
-                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
-            return
-        sig = codegen.stmt_sig(ps, 3)
-        src, name, block, smem, wgeo = wavefront.source(sig, info.dtype, cfg)
-        kern = self.dev.kernel(src, name, block, smem)
-        tmA = self._tmap(ba, wgeo["box"], cfg.l2promo)
-        tmB = self._tmap(bb, wgeo["box"], cfg.l2promo)
-        params = wavefront.pack_params(tmA, tmB, ba.addr(*s_lo), bb.addr(*s_lo), ptr, ba.py, ba.pz,
-                                       ba.xoff + s_lo[2], s_lo[1], s_lo[0], geo)
-        occ = self.dev.occupancy(kern)
-        if occ < 1:
-            raise RuntimeError("wave kernel cannot be resident on this device")
-        self._recording = [] if ck is not None else None
-        try:
-            self._launch(kern, (self.dev.sm_count, 1, 1), params, tag=("tb", 2))
-        finally:
-            rec, self._recording = self._recording, None
-        if ck is not None and rec is not None:
-            self._launches[ck] = rec
-
-    def _launch_resident(self, node, plan, sweeps: int, key) -> None:
-        """One persistent launch running `sweeps` ping-pong sweeps in L2."""
-        ps = plan.statements[0]
-        a, b = ps.inputs[0], ps.output
-        tile = next(iter(self.store.tiles.values()))
-        ba, bb = tile.buffers[a], tile.buffers[b]
-        info = self.store.arrays[a]
-        if not self._bar:
-            self._bar = self.dev.alloc(256)
-        self.dev.memset_zero(self._bar, 4, COMPUTE)
-        ck = (key, node.node_id, self.store.version, "res") if key is not None else None
-        rec = self._launches.get(ck) if ck is not None else None
-        if rec is not None and not self.time_kernels:
-            for kern, grid, params in rec:
-                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
-            return
-        sig = codegen.stmt_sig(ps, info.rank)
-        src, name, block, smem, geo = resident.source(sig, info.dtype, info.rank)
-        kern = self.dev.kernel(src, name, block, 0)
-        d = (0,) * (3 - info.rank) + tuple(ba.depth[3 - info.rank:])
-        bounds = ((0, 1),) * (3 - info.rank) + tuple(ps.output_slice_bounds)
-        s_lo = tuple(lo + dd for (lo, _), dd in zip(bounds, d))
-        s_hi = tuple(hi + dd for (_, hi), dd in zip(bounds, d))
-        org = ba.xoff * ba.elem
-        params = resident.pack_params(ba.ptr + org, bb.ptr + org, self._bar, ba, s_lo, s_hi, sweeps, geo)
-        # every CTA must be co-resident (grid barrier): size by measured occupancy
-        occ = self.dev.occupancy(kern)
-        if occ < 1:
-            raise RuntimeError("resident chain kernel cannot be resident on this device")
-        cfg = geo["cfg"]
-        n_tiles = 1
-        for lo, hi, t in zip(s_lo, s_hi, (cfg.tz, cfg.ty, cfg.tx)):
-            n_tiles *= -(-(hi - lo) // t)
-        grid = (max(1, min(self.dev.sm_count * min(geo["min_blocks"], occ), n_tiles)), 1, 1)
-        self._recording = [] if ck is not None else None
-        try:
-            self._launch(kern, grid, params, tag=("res", sweeps))
-        finally:
-            rec, self._recording = self._recording, None
-        if ck is not None and rec is not None:
-            self._launches[ck] = rec
 
     def _rsm_geometry(self, c, sig):
         (y0, y1), (x0, x1) = c[2]
@@ -525,8 +445,8 @@ class GpuExecutor:
         ck = (key, node.node_id, self.store.version, "rsm") if key is not None else None
         rec = self._launches.get(ck) if ck is not None else None
         if rec is not None and not self.time_kernels:
-            for kern, grid, params in rec:
-                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
+            for kern, grid, params, coop in rec:
+                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None, coop)
             return
         sig = codegen.stmt_sig(ps, 2)
         c = self._chain_candidate(plan)
@@ -543,7 +463,7 @@ class GpuExecutor:
             raise RuntimeError("resident-smem chain kernel cannot be resident on this device")
         self._recording = [] if ck is not None else None
         try:
-            self._launch(kern, grid, params, tag=("rsm", sweeps))
+            self._launch(kern, grid, params, tag=("rsm", sweeps), cooperative=True)
         finally:
             rec, self._recording = self._recording, None
         if ck is not None and rec is not None:
@@ -580,14 +500,15 @@ class GpuExecutor:
         ck = (key, node.node_id, self.store.version, "tb") if key is not None else None
         rec = self._launches.get(ck) if ck is not None else None
         if rec is not None and not self.time_kernels:
-            for kern, grid, params in rec:
-                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
+            for kern, grid, params, coop in rec:
+                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None, coop)
             return
         src_buf, dst_buf = (home, twin) if ch % 2 == 0 else (twin, home)
         sig = codegen.stmt_sig(ps, 3)
-        src, name, block, smem, lay = temporal.source(sig, self.store.arrays[a].dtype, self.tb_cfg)
+        src, name, block, smem, lay = temporal.source(sig, self.store.arrays[a].dtype, self.tb_cfg,
+                                                      py=home.py, pz=home.pz, xoff=home.xoff)
         kern = self.dev.kernel(src, name, block, smem)
-        geo = temporal.item_geometry(s_lo, s_hi, self.dev.sm_count, lay)
+        geo = temporal.item_geometry(s_lo, s_hi, self.dev.sm_count, lay, xoff=home.xoff)
         tm = self._tmap(src_buf, (lay["w0"], lay["h0"], 1), self.tb_cfg.l2promo)
         org = home.xoff * home.elem
         params = temporal.pack_params(tm, src_buf.ptr + org, bbuf.ptr + org, dst_buf.ptr + org,
@@ -654,8 +575,8 @@ class GpuExecutor:
         ck = (key, node.node_id, self.store.version, zsplit) if key is not None else None
         recorded = self._launches.get(ck) if ck is not None else None
         if recorded is not None and not self.time_kernels:
-            for kern, grid, params in recorded:
-                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
+            for kern, grid, params, coop in recorded:
+                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None, coop)
             return
         self._recording = [] if ck is not None else None
         try:
@@ -667,18 +588,20 @@ class GpuExecutor:
                 self._launches.clear()
             self._launches[ck] = rec
 
-    def _launch(self, kern, grid, params, tag=("node", 1)) -> None:
-        """`tag` = (kernel kind, sweeps covered) for the timing records."""
+    def _launch(self, kern, grid, params, tag=("node", 1), cooperative: bool = False) -> None:
+        """`tag` = (kernel kind, sweeps covered) for the timing records;
+        `cooperative` for grid-barrier kernels (co-residency guaranteed by the
+        driver, or the launch fails)."""
         if self._recording is not None:
-            self._recording.append((kern, grid, params))
+            self._recording.append((kern, grid, params, cooperative))
         if self.time_kernels:
             ev0, ev1 = self.dev.event(), self.dev.event()
             ev0.record(COMPUTE)
-            self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
+            self.dev.launch(kern, grid, params, COMPUTE, self.transport is None, cooperative)
             ev1.record(COMPUTE)
             self.kernel_events.append((ev0, ev1, tag))
         else:
-            self.dev.launch(kern, grid, params, COMPUTE, self.transport is None)
+            self.dev.launch(kern, grid, params, COMPUTE, self.transport is None, cooperative)
 
     def _subboxes(self, zsplit, geom, rank: int, tile, ps, local, n3) -> list:
         """Sub-boxes (offset (z, y, x) within the box, extents) to launch: the

@@ -4,30 +4,50 @@ A batch of heat/Jacobi iterations is a chain of single-statement rank-3 nodes
 `B[S] = f(A[S + offsets]); A[S] = f(B[S + offsets]); ...` (SURVEY.md §8f row 2;
 reference semantics executor.py:258-348: nodes run in order, statement at a
 time). On one GPU with one tile no halo exchange happens between them, so K of
-them (K even) can run as ONE kernel that reads A once from HBM, keeps the
-intermediate sweeps in shared memory and writes only the arrays' final values:
-24 B per K updates instead of 16 B per update (12 B/LUP at K = 2).
+them (K even) run as ONE kernel that reads A once from HBM, keeps the
+intermediate sweeps on chip and writes only the arrays' final values: A read
+and A written once per K sweeps, B written only by a run's last chain
+(`write_b`), i.e. 8 B/LUP for fp64 at K = 2 instead of 16 B/LUP for single
+sweeps.
 
-Every point is still computed by the same generated expression
-(codegen._emit_expr: one correctly rounded IEEE op per plan instruction, no
-contraction), so results are bit-identical to K separate sweeps. Epochs,
-rounds and launch counts are kept per node by the executor.
+Every point is computed by the generated expression of codegen._emit_expr
+(one correctly rounded IEEE op per plan instruction, no contraction), so the
+results are bit-identical to K separate sweeps. Epochs, rounds and launch
+counts are kept per node by the executor.
 
-Kernel structure (warp-specialised like stream.source_ws2):
-* work item = a BX x BY output column of S over ZC planes; step j (1..K) of
-  the chain covers the item tile expanded by (K-j)*r in y/x (overlapped
-  tiling) and trails step j-1 by rz planes in z;
-* producer warp: one TMA (`cp.async.bulk.tensor.3d`) per input plane of A
-  (tile + K*r halo) into an mbarrier-gated ring (full/empty barriers);
-* compute warps, per input plane: step 1 reads the TMA ring, step j > 1 reads
-  step j-1's shared-memory plane ring (2rz+2 planes); one named barrier
-  between steps. Cells of a step's region outside S keep the array's stored
-  value (read from its home buffer; S's complement is never written);
-* stores: step K-1 (array B, final) in place inside S; step K (array A,
-  final) into A's *other* home buffer, because neighbouring CTAs still read A
-  through TMA. The executor alternates A between its tile buffer and a
-  scratch twin (chains come in pairs, so A ends in its own buffer) and copies
-  S's complement into the twin at the start of each run.
+Kernel structure (one warp-specialised, persistent CTA per SM):
+
+* work item = a BX x BY output column of S over a z-chunk of ZC planes
+  (chunks balanced so every item has the same depth); x tiles start at a
+  16-byte aligned padded column so every thread's V = 16/elem consecutive
+  points are one 128-bit vector (fp64 pairs, fp32 quads) in shared memory and
+  in HBM;
+* step j (1..K) covers the tile expanded by m_j columns / (K-j)*ry rows
+  (overlapped tiling; m_j rounded up to V) and trails step j-1 by rz planes;
+* producer warp: one elected lane issues one TMA (`cp.async.bulk.tensor.3d`)
+  per input plane (tile + halo) into an mbarrier ring (full/empty barriers),
+  running ahead into the next item;
+* compute threads: thread (c, g) owns vector column c and RPT consecutive
+  rows of the step-1 frame for every step and every plane. Its z-window of
+  every step (2rz+1 planes) lives in registers and rotates by renaming (the
+  plane loop is unrolled 2rz+1 times); in-plane neighbours come from shared
+  memory: the TMA plane for step 1, step j's plane ring (rz+1 slots, the
+  step-1 frame) for step j+1. Per plane a thread does one mbarrier wait, its
+  vector loads / expressions / one vector store per row and step, and ONE
+  named barrier; one thread releases the input slot after that barrier;
+* items whose step-1 frame lies inside S in y/x take a predicate-free path;
+  edge items keep the array's stored value at points outside S (prefetched
+  before the plane's mbarrier wait) and store per component;
+* stores: step K-1 (array B, final) in place, only in a run's last chain;
+  step K (array A, final) into A's *other* home buffer, because neighbouring
+  CTAs still read A through TMA. The executor alternates A between its tile
+  buffer and a scratch twin (chains come in pairs, so A ends in its own
+  buffer) and copies S's complement into the twin at the start of each run.
+
+Earlier variants (a 2-row-per-thread scalar kernel with per-step mbarrier
+rings, a warp-shuffle variant, an L2-forwarded wavefront and an L2-resident
+grid-barrier chain) were measured slower and removed; their numbers are in
+profiles/r1_tb_sweep.md and profiles/r1s2_tb_skipb.md.
 """
 
 from __future__ import annotations
@@ -40,7 +60,7 @@ from .codegen import CTYPE, ELEM, StmtSig, _emit_expr, slot_radius
 from .stream import _PTX_HELPERS
 
 MAX_RADIUS = 2
-SMEM_BUDGET = 200 * 1024
+SMEM_BUDGET = 220 * 1024
 SMEM_PER_SM = 228 * 1024
 SKIP_MID_B = os.environ.get("EST_TB_SKIPB", "1") == "1"
 
@@ -48,18 +68,13 @@ SKIP_MID_B = os.environ.get("EST_TB_SKIPB", "1") == "1"
 @dataclass(frozen=True)
 class TbCfg:
     k: int = 2              # sweeps per launch (even)
-    bx: int = 48            # output columns per item
+    bx: int = 64            # output columns per item (multiple of 16/elem)
     by: int = 32            # output rows per item
-    rpt: int = 2            # rows of the step-1 region per compute thread
+    rpt: int = 2            # consecutive step-1-frame rows per compute thread
     prefetch: int = 2       # input planes in flight beyond the z window
-    zchunk: int = 192       # planes per item (C4: 5 full chunks + 62; 1-2 % over 128, profiles/r1s2_tb_skipb.md)
+    zchunk: int = 192       # target planes per item (chunks are balanced)
     l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
-    persistent: bool = False
-    minb: int = 0           # __launch_bounds__ min blocks per SM (0: from smem/threads, >= 48 regs)
-    variant: str = "block"  # "block" (smem ring per step) or "warp" (intermediate sweep in registers + shuffles)
-    wx: int = 2             # (warp) warps across x; each warp owns 30 output columns
-    wy: int = 4             # (warp) warps across y
-    r: int = 4              # (warp) output rows per warp
+    persistent: bool = True  # one CTA per SM slot looping over items
 
 
 def _env_cfg() -> TbCfg:
@@ -68,19 +83,16 @@ def _env_cfg() -> TbCfg:
     return TbCfg(k=int(e("EST_TB_K", d.k)), bx=int(e("EST_TB_BX", d.bx)), by=int(e("EST_TB_BY", d.by)),
                  rpt=int(e("EST_TB_RPT", d.rpt)), prefetch=int(e("EST_TB_PREFETCH", d.prefetch)),
                  zchunk=int(e("EST_TB_ZCHUNK", d.zchunk)), l2promo=int(e("EST_TB_L2PROMO", d.l2promo)),
-                 persistent=e("EST_TB_PERSISTENT", "0") == "1", minb=int(e("EST_TB_MINB", d.minb)),
-                 variant=e("EST_TB_VARIANT", d.variant), wx=int(e("EST_TB_WX", d.wx)),
-                 wy=int(e("EST_TB_WY", d.wy)), r=int(e("EST_TB_R", d.r)))
+                 persistent=e("EST_TB_PERSISTENT", "1") == "1")
 
 
 DEFAULT = _env_cfg()
 ENABLED = os.environ.get("EST_TB", "1") == "1"
-# measured crossover (profiles/r1s2_tb_skipb.md): at 1022^3 outputs the chain
-# beats two single sweeps by 18 %, at 510^3 it is 1.5-4 % slower (too few
-# items per SM to hide each item's pipeline fill)
-MIN_POINTS = int(os.environ.get("EST_TB_MIN_POINTS", 1 << 28))
+# chains are scheduled from this many output points (smaller grids: too few
+# items per SM to hide each item's pipeline fill; see DESIGN.md)
+MIN_POINTS = int(os.environ.get("EST_TB_MIN_POINTS", 1 << 26))
 # chain depths that passed the GPU parity suite (EST_TB_VALIDATED_K widens it for experiments)
-VALIDATED_K = tuple(int(k) for k in os.environ.get("EST_TB_VALIDATED_K", "2").split(","))
+VALIDATED_K = tuple(int(k) for k in os.environ.get("EST_TB_VALIDATED_K", "2,4").split(","))
 
 
 def _round(v: int, m: int) -> int:
@@ -93,57 +105,57 @@ def z_star(st: StmtSig) -> bool:
 
 
 def layout(rad, dtype: int, cfg: TbCfg) -> dict:
-    """Shared memory: the input TMA ring (tile + K*r halo) and, per
-    intermediate step, a ring of 2rz+2 planes in the step-1 frame (W1 x H1)
-    with one mbarrier per plane slot (count = compute warps)."""
+    """Frames, margins, thread grid and shared memory of the chain kernel.
+
+    x margins m_j (columns each side of the output tile that step j computes)
+    are rounded to the vector width V so every frame starts on a vector; y
+    margins are e_j = (K-j)*ry. Frame 0 is the TMA input plane, frames 1..K-1
+    are the intermediate steps' plane rings (all in the step-1 geometry)."""
     rz, ry, rx = rad
     elem = ELEM[dtype]
-    q = 16 // elem
+    V = 16 // elem
     K = cfg.k
-    w0 = _round(cfg.bx + 2 * K * rx + q - 1, q)
-    h0 = cfg.by + 2 * K * ry
+    m = [0] * (K + 1)
+    for j in range(K - 1, -1, -1):
+        m[j] = _round(m[j + 1] + rx, V)
+    e = [(K - j) * ry for j in range(K + 1)]
+    W0, H0 = cfg.bx + 2 * m[0], cfg.by + 2 * e[0]
+    W1, H1 = cfg.bx + 2 * m[1], cfg.by + 2 * e[1]
+    P1 = W1 // V
+    G1 = -(-H1 // cfg.rpt)
+    nact = P1 * G1
+    NT = _round(nact, 32)
+    Z = 2 * rz + 1
     s0 = rz + 1 + cfg.prefetch
-    pl0 = _round(w0 * h0 * elem, 1024)
-    w1, h1 = cfg.bx + 2 * (K - 1) * rx, cfg.by + 2 * (K - 1) * ry
-    pl1 = _round(w1 * h1 * elem, 128)
-    off = s0 * pl0
+    # every thread (active or not) computes its whole footprint unpredicated:
+    # the frames are padded with the rows the last row group reads
+    rows_t = -(-NT // P1) * cfg.rpt
+    pl0 = _round(W0 * max(H0, (e[0] - e[1]) + rows_t + ry) * elem + 2 * elem * V, 128)
+    pl1 = _round(W1 * max(H1, rows_t + ry) * elem + 2 * elem * V, 128)
     rings = []
-    nr = 2 * rz + 2  # slots: a warp may run one plane ahead (split arrive / wait)
+    off = s0 * pl0
+    R = rz + 1  # plane slots per intermediate ring (written at t, read rz iterations later)
     for _j in range(1, K):
-        rings.append({"off": off, "n": nr})
-        off += nr * pl1
+        rings.append(off)
+        off += R * pl1
     data = _round(off, 8)
-    smem = data + 8 * (2 * s0 + (K - 1) * nr) + 1024
-    hg = h1 // cfg.rpt if h1 % cfg.rpt == 0 else 0
-    nt = _round(w1 * hg, 32)
-    return {"rad": (rz, ry, rx), "w0": w0, "h0": h0, "s0": s0, "pl0": pl0, "w1": w1, "h1": h1,
-            "pl1": pl1, "hg": hg, "nt": nt, "rings": rings, "data": data, "smem": smem,
-            "cfg": cfg, "elem": elem, "q": q}
-
-
-def warp_eligible(st: StmtSig, dtype: int, cfg: TbCfg) -> bool:
-    """Warp-tiled variant: K = 2, one input slot, every offset within +-1, z-star."""
-    if cfg.variant != "warp" or cfg.k != 2 or st.arity != 1 or dtype not in ELEM or not z_star(st):
-        return False
-    rad = slot_radius(st).get(0)
-    return rad is not None and max(rad) <= 1 and rad[0] == 1 and cfg.r >= 1
+    smem = data + 8 * 2 * s0 + 1024
+    return {"rad": (rz, ry, rx), "V": V, "m": m, "e": e, "w0": W0, "h0": H0, "w1": W1, "h1": H1,
+            "p1": P1, "g1": G1, "nact": nact, "nt": NT, "Z": Z, "R": R, "s0": s0, "pl0": pl0, "pl1": pl1,
+            "rings": rings, "data": data, "smem": smem, "cfg": cfg, "elem": elem, "bx": cfg.bx, "by": cfg.by}
 
 
 def eligible(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> bool:
     """Single input slot, z-star loads, 1 <= rz, radius <= MAX_RADIUS, fits."""
     cfg = cfg or DEFAULT
-    if warp_eligible(st, dtype, cfg):
-        return True
-    # K = 4 chains are bit-exact since the padded-z guard of the fast path
-    # (scripts/debug_tb_k4.py) but 1.5-1.7x slower than K = 2 on C4
-    # (profiles/r1s2_tb_skipb.md), so only K = 2 is scheduled by default
-    if cfg.k not in VALIDATED_K or st.arity != 1 or dtype not in ELEM or not z_star(st):
+    if (cfg.k not in VALIDATED_K or cfg.k % 2 or st.arity != 1 or dtype not in ELEM or not z_star(st)
+            or cfg.bx % (16 // ELEM.get(dtype, 8))):
         return False
     rad = slot_radius(st).get(0)
     if rad is None or max(rad) > MAX_RADIUS or rad[0] < 1:
         return False
     lay = layout(rad, dtype, cfg)
-    if lay["w0"] > 256 or lay["h0"] > 256 or lay["hg"] == 0 or lay["nt"] + 32 > 1024:
+    if lay["w0"] > 256 or lay["h0"] > 256 or lay["nt"] + 32 > 1024:
         return False
     return lay["smem"] <= SMEM_BUDGET
 
@@ -152,531 +164,329 @@ def blocks_per_sm(smem: int, nt: int) -> int:
     return max(1, min(SMEM_PER_SM // (smem + 1024), 2048 // (nt + 32)))
 
 
-def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
-    cfg = cfg or DEFAULT
-    if warp_eligible(st, dtype, cfg):
-        return source_warp(st, dtype, cfg)
-    return source_block(st, dtype, cfg)
+class _Emitter:
+    """Source text builder for one (statement, dtype, cfg, buffer layout) chain kernel."""
+
+    def __init__(self, st: StmtSig, dtype: int, lay: dict, py: int, pz: int, xoff: int):
+        self.st, self.dtype, self.lay = st, dtype, lay
+        self.py, self.pz, self.xoff = py, pz, xoff
+        self.T = CTYPE[dtype]
+        self.VT = {8: "double2", 4: "float4"}[lay["elem"]]
+        self.L: list = []
+
+    def a(self, s: str) -> None:
+        self.L.append(s)
+
+    @staticmethod
+    def _rn(x: int) -> str:
+        return f"m{-x}" if x < 0 else str(x)
+
+    def step_body(self, j: int, mm: int) -> tuple:
+        """Expression lines of step j for every (row, component) of the
+        thread at unroll position mm, and the shared-memory operands they
+        need, grouped by (thread-relative row, vector group)."""
+        lay = self.lay
+        V, RPT, Z = lay["V"], lay["cfg"].rpt, lay["Z"]
+        rz = lay["rad"][0]
+        need: dict = {}
+        body = []
+        for r in range(RPT):
+            for v in range(V):
+                def load(slot, off3, r=r, v=v):
+                    dz, dy, dx = off3
+                    if dz != 0 or (dy == 0 and dx == 0):
+                        return f"c{j - 1}_{r}_{v}_{(rz + dz + mm) % Z}"
+                    rr, xc = r + dy, v + dx
+                    if 0 <= rr < RPT and 0 <= xc < V:
+                        return f"c{j - 1}_{rr}_{xc}_{(rz + mm) % Z}"
+                    g, comp = xc // V, xc % V
+                    need.setdefault((rr, g), set()).add(comp)
+                    return f"n_{self._rn(rr)}_{self._rn(g)}_{comp}"
+                lines, res = _emit_expr(self.st, self.dtype, load)
+                body.append((r, v, lines, res))
+        return body, need
+
+    def emit_smem_loads(self, ind: str, need: dict, base: str, pitch: int) -> None:
+        """One vector load per group with >= 2 needed components, else scalars."""
+        V = self.lay["V"]
+        for (rr, g), comps in sorted(need.items()):
+            off = rr * pitch + g * V
+            tag = f"{self._rn(rr)}_{self._rn(g)}"
+            if len(comps) >= 2:
+                self.a(f"{ind}const {self.VT} q_{tag} = *reinterpret_cast<const {self.VT}*>({base} + ({off}));")
+                for c in sorted(comps):
+                    self.a(f"{ind}const {self.T} n_{tag}_{c} = q_{tag}.{'xyzw'[c]};")
+            else:
+                (c,) = tuple(comps)
+                self.a(f"{ind}const {self.T} n_{tag}_{c} = {base}[{off + c}];")
+
+    # -- kernel ---------------------------------------------------------------
+    def source(self) -> str:
+        lay = self.lay
+        cfg = lay["cfg"]
+        K, RPT, V, Z = cfg.k, cfg.rpt, lay["V"], lay["Z"]
+        rz = lay["rad"][0]
+        m, e = lay["m"], lay["e"]
+        W0, H0, W1, H1, P1 = lay["w0"], lay["h0"], lay["w1"], lay["h1"], lay["p1"]
+        NT, s0, E = lay["nt"], lay["s0"], lay["elem"]
+        a = self.a
+        NW = NT // 32
+        minb = max(1, min(blocks_per_sm(lay["smem"], NT), 65536 // ((NT + 32) * 80)))
+        lay["min_blocks"] = minb
+        a(f'// generated by paper_2512_19851_b200/temporal.py — skeleton "tb" (K={K} fused sweeps, '
+          f'V={V} vectors) {cfg} py={self.py} pz={self.pz} xoff={self.xoff}')
+        a(f"typedef {self.T} T;")
+        a("struct __align__(64) Tmap { unsigned long long w[16]; };")
+        a("struct __align__(64) Params { Tmap tm;")
+        a("  unsigned long long src, bhome, adst;  // padded-box origins: A now, B (in place), A next")
+        a("  int npz, npy, npx, sz0, sz1, sy0, sy1, sx0, sx1, xt0, nbx, nby, zc, nzc, wb; };")
+        a(_PTX_HELPERS)
+        a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
+        a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
+        a("__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {")
+        a("  unsigned ok; asm volatile(\"{\\n .reg .pred p;\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\\n\"")
+        a("  \" selp.u32 %0, 1, 0, p;\\n}\" : \"=r\"(ok) : \"r\"(smem_u32(b)), \"r\"(parity) : \"memory\"); return ok; }")
+        a("__device__ __forceinline__ void mbar_wait2(unsigned long long* b, unsigned parity) {")
+        a("  if (!mbar_try(b, parity)) mbar_wait(b, parity); }  // fast first probe, bounded slow path")
+        a(f'extern "C" __global__ void __launch_bounds__({NT + 32}, {minb})')
+        a("est_tb(const __grid_constant__ Params p) {")
+        a("  extern __shared__ __align__(1024) unsigned char smem[];")
+        a(f"  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + {lay['data']});")
+        a(f"  unsigned long long* empty = full + {s0};")
+        a("  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;")
+        a("  const int n_items = p.nbx * p.nby * p.nzc;")
+        a("  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");")
+        a("  if (tid == 0) {")
+        a(f"    for (int i = 0; i < {s0}; ++i) {{ mbar_init(full + i, 1); mbar_init(empty + i, 1); }}")
+        a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
+        a("  }")
+        a("  __syncthreads();")
+        a("  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");  // the previous chain's stores are visible")
+
+        def item_decode(ind):
+            a(f"{ind}const int bx = item % p.nbx, rest = item / p.nbx;")
+            a(f"{ind}const int by = rest % p.nby, bzc = rest / p.nby;")
+            a(f"{ind}const int x0 = p.xt0 + bx * {cfg.bx}, y0 = p.sy0 + by * {cfg.by};")
+            a(f"{ind}const int zs = p.sz0 + bzc * p.zc;")
+            a(f"{ind}const int nzl = min(p.zc, p.sz1 - zs);")
+            a(f"{ind}const int n0 = nzl + {2 * K * rz};")
+
+        # ---------------- producer warp
+        a(f"  if (warp == {NW}) {{")
+        a("    if (lane != 0) return;")
+        a("    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm) : \"memory\");")
+        a("    int fill = 0;")
+        a("    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+        item_decode("      ")
+        a("      for (int k = 0; k < n0; ++k) {")
+        a(f"        const int g = fill + k, stg = g % {s0};")
+        a(f"        if (g >= {s0}) mbar_wait(empty + stg, ((g / {s0}) - 1) & 1);")
+        a(f"        mbar_expect(full + stg, {W0 * H0 * E});")
+        a(f"        tma_load3(smem + stg * {lay['pl0']}, &p.tm, x0 + {self.xoff - m[0]}, y0 - {e[0]}, "
+          f"zs - {K * rz} + k, full + stg);")
+        a("      }")
+        a("      fill += n0;")
+        a("    }")
+        a("    return;")
+        a("  }")
+        # ---------------- compute threads
+        a("  const T* __restrict__ asrc = reinterpret_cast<const T*>(p.src);")
+        a("  T* __restrict__ bmem = reinterpret_cast<T*>(p.bhome);")
+        a("  T* __restrict__ adst = reinterpret_cast<T*>(p.adst);")
+        a(f"  const bool act = tid < {lay['nact']};")
+        a(f"  const int cc = tid % {P1}, gg = tid / {P1};  // vector column / row group in the step-1 frame")
+        a(f"  const int off0 = ({e[0] - e[1]} + gg * {RPT}) * {W0} + {m[0] - m[1]} + cc * {V};  // input frame")
+        a(f"  const int off1 = gg * {RPT} * {W1} + cc * {V};  // step-1 frame (rings)")
+        for j in range(1, K + 1):
+            dm, de = (m[1] - m[j]) // V, e[1] - e[j]
+            for r in range(RPT):
+                a(f"  const bool in{j}_{r} = act && (gg * {RPT} + {r}) >= {de} && (gg * {RPT} + {r}) < {H1 - de}"
+                  f" && cc >= {dm} && cc < {P1 - dm};")
+        for j in range(0, K):
+            for r in range(RPT):
+                for v in range(V):
+                    a(f"  T {', '.join(f'c{j}_{r}_{v}_{k} = 0' for k in range(Z))};")
+        a("  int is = 0, ip = 0;  // input ring slot / phase of plane t")
+        a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
+        item_decode("    ")
+        a(f"    const long long gb = (long long)(y0 - {e[1]} + gg * {RPT}) * {self.py} + (x0 - {m[1]} + cc * {V});")
+        a(f"    const bool fast = (x0 - {m[1]} >= p.sx0) && (x0 + {cfg.bx + m[1]} <= p.sx1) &&"
+          f" (y0 - {e[1]} >= p.sy0) && (y0 + {cfg.by + e[1]} <= p.sy1);")
+        a("    if (fast) {")
+        self.emit_loop("      ", edge=False)
+        a("    } else {")
+        # per-thread S / padded-box predicates of the item (edge items only)
+        for r in range(RPT):
+            a(f"      const int gy{r} = y0 - {e[1]} + gg * {RPT} + {r};")
+            a(f"      const bool ys{r} = gy{r} >= p.sy0 && gy{r} < p.sy1, yp{r} = gy{r} >= 0 && gy{r} < p.npy;")
+        for v in range(V):
+            a(f"      const int gx{v} = x0 - {m[1]} + cc * {V} + {v};")
+            a(f"      const bool xs{v} = gx{v} >= p.sx0 && gx{v} < p.sx1, xp{v} = gx{v} >= 0 && gx{v} < p.npx;")
+        self.emit_loop("      ", edge=True)
+        a("    }")
+        a("  }")
+        a("}")
+        return "\n".join(self.L) + "\n"
+
+    def emit_loop(self, ind: str, edge: bool) -> None:
+        """The plane loop of one item, unrolled Z = 2rz+1 times (register
+        windows rotate by renaming). Every thread computes every row and
+        component of its footprint (no divergent branches; frames are padded
+        so out-of-region operands stay inside shared memory); only stores
+        and global loads are predicated."""
+        lay = self.lay
+        cfg = lay["cfg"]
+        K, RPT, V, Z = cfg.k, cfg.rpt, lay["V"], lay["Z"]
+        rz = lay["rad"][0]
+        W0, W1, s0, E = lay["w0"], lay["w1"], lay["s0"], lay["elem"]
+        pl0, pl1 = lay["pl0"] // E, lay["pl1"] // E
+        PY, PZ = self.py, self.pz
+        NT = lay["nt"]
+        VT = self.VT
+        a = self.a
+        a(f"{ind}T* ap = adst + (long long)zs * {PZ} + gb;  // step-K plane (A next)")
+        a(f"{ind}T* bp = bmem + (long long)(zs - {rz}) * {PZ} + gb;  // step-(K-1) plane (B)")
+        a(f"{ind}const T* ring0 = reinterpret_cast<const T*>(smem);")
+        a(f"{ind}int tr = 0;  // t mod R (intermediate ring slots)")
+        a(f"{ind}for (int t0 = 0; t0 < n0; t0 += {Z}) {{")
+        for mm in range(Z):
+            i2 = ind + "  "
+            a(f"{i2}if (t0 + {mm} < n0) {{  // plane iteration t = t0 + {mm}")
+            i3 = i2 + "  "
+            a(f"{i3}const int t = t0 + {mm};")
+            for j in range(1, K):
+                a(f"{i3}const int u{j} = zs - {(K + j) * rz} + t;  // step-{j} plane")
+                a(f"{i3}const bool zs{j} = u{j} >= p.sz0 && u{j} < p.sz1, zp{j} = u{j} >= 0 && u{j} < p.npz;")
+                if edge:
+                    # stored values outside S, prefetched before the plane's wait
+                    home = "bmem" if j % 2 == 1 else "asrc"
+                    for r in range(RPT):
+                        for v in range(V):
+                            a(f"{i3}T h{j}_{r}_{v} = (T)0;")
+                            a(f"{i3}if (t >= {2 * j * rz} && in{j}_{r} && zp{j} && yp{r} && xp{v} && "
+                              f"!(zs{j} && ys{r} && xs{v})) h{j}_{r}_{v} = "
+                              f"{home}[(long long)u{j} * {PZ} + gb + {r * PY + v}];")
+            a(f"{i3}mbar_wait2(full + is, ip);")
+            a(f"{i3}{{ const T* S0 = ring0 + is * {pl0} + off0;  // own points of input plane t")
+            for r in range(RPT):
+                a(f"{i3}  {{ const {VT} q = *reinterpret_cast<const {VT}*>(S0 + {r * W0});")
+                a(f"{i3}    " + " ".join(f"c0_{r}_{v}_{(2 * rz + mm) % Z} = q.{'xyzw'[v]};" for v in range(V)) + " }")
+            a(f"{i3}}}")
+            a(f"{i3}int ir = is - {rz}; if (ir < 0) ir += {s0};  // slot of plane t - rz")
+            for j in range(1, K + 1):
+                final = j == K
+                a(f"{i3}if (t >= {2 * j * rz}) {{  // step {j}")
+                i4 = i3 + "  "
+                if j == 1:
+                    a(f"{i4}const T* P = ring0 + ir * {pl0} + off0;")
+                    pitch = W0
+                else:
+                    R = lay["R"]
+                    c = (rz + 2 * (j - 1) * rz) % R
+                    a(f"{i4}int rs = tr - {c}; if (rs < 0) rs += {R};  // ring {j - 1} slot of plane u{j}")
+                    a(f"{i4}const T* P = reinterpret_cast<const T*>(smem + {lay['rings'][j - 2]}) + "
+                      f"rs * {pl1} + off1;")
+                    pitch = W1
+                if not final:
+                    R = lay["R"]
+                    c = (2 * j * rz) % R
+                    a(f"{i4}int ws = tr - {c}; if (ws < 0) ws += {R};  // ring {j} slot of plane u{j}")
+                    a(f"{i4}T* Wr = reinterpret_cast<T*>(smem + {lay['rings'][j - 1]}) + ws * {pl1} + off1;")
+                    a(f"{i4}if (zs{j}) {{")
+                else:
+                    a(f"{i4}{{")
+                i5 = i4 + "  "
+                body, need = self.step_body(j, mm)
+                self.emit_smem_loads(i5, need, "P", pitch)
+                for r, v, lines, res in body:
+                    a(f"{i5}T o{r}_{v};")
+                    a(f"{i5}{{ " + " ".join(lines) + f" o{r}_{v} = {res}; }}")
+                for r in range(RPT):
+                    outs = [f"o{r}_{v}" for v in range(V)]
+                    if edge and not final:
+                        for v in range(V):
+                            a(f"{i5}if (!(ys{r} && xs{v})) o{r}_{v} = h{j}_{r}_{v};")
+                    vec = f"make_{VT}({', '.join(outs)})"
+                    if not final:
+                        a(f"{i5}*reinterpret_cast<{VT}*>(Wr + {r * W1}) = {vec};")
+                        a(f"{i5}" + " ".join(f"c{j}_{r}_{v}_{(2 * rz + mm) % Z} = o{r}_{v};" for v in range(V)))
+                    targets = []
+                    if final:
+                        targets.append(("ap", f"in{K}_{r}"))
+                    if j == K - 1:
+                        targets.append(("bp", f"p.wb && in{K}_{r} && u{j} >= zs && u{j} < zs + nzl"))
+                    for ptr, cond in targets:
+                        if not edge:
+                            a(f"{i5}if ({cond}) *reinterpret_cast<{VT}*>({ptr} + {r * PY}) = {vec};")
+                        else:
+                            allin = " && ".join(f"xs{v}" for v in range(V))
+                            a(f"{i5}if ({cond} && ys{r}) {{")
+                            a(f"{i5}  if ({allin}) *reinterpret_cast<{VT}*>({ptr} + {r * PY}) = {vec};")
+                            a(f"{i5}  else {{ " + " ".join(f"if (xs{v}) {ptr}[{r * PY + v}] = o{r}_{v};"
+                                                          for v in range(V)) + " }")
+                            a(f"{i5}}}")
+                a(f"{i4}}}")
+                if not final:
+                    # plane outside S: the array's stored value (0 beyond the padded box)
+                    home = "bmem" if j % 2 == 1 else "asrc"
+                    a(f"{i4}else {{")
+                    for r in range(RPT):
+                        vals = []
+                        for v in range(V):
+                            a(f"{i4}  const T s{r}_{v} = (zp{j} && in{j}_{r}) ? "
+                              f"{home}[(long long)u{j} * {PZ} + gb + {r * PY + v}] : (T)0;")
+                            vals.append(f"s{r}_{v}")
+                        a(f"{i4}  *reinterpret_cast<{VT}*>(Wr + {r * W1}) = make_{VT}({', '.join(vals)});")
+                        a(f"{i4}  " + " ".join(f"c{j}_{r}_{v}_{(2 * rz + mm) % Z} = s{r}_{v};" for v in range(V)))
+                    a(f"{i4}}}")
+                if final:
+                    a(f"{i4}ap += {PZ};")
+                if j == K - 1:
+                    a(f"{i4}bp += {PZ};")
+                a(f"{i3}}}")
+            a(f"{i3}asm volatile(\"bar.sync 1, {NT};\" ::: \"memory\");")
+            a(f"{i3}if (tid == 0 && t >= {rz}) mbar_arrive(empty + ir);  // plane t - rz fully consumed")
+            a(f"{i3}if (++is == {s0}) {{ is = 0; ip ^= 1; }}")
+            if K > 1:
+                a(f"{i3}if (++tr == {lay['R']}) tr = 0;")
+            a(f"{i2}}}")
+        a(f"{ind}}}")
+        # planes never used as a step-1 centre plane in this item: release their slots
+        a(f"{ind}if (tid == 0) for (int k = (n0 > {rz} ? n0 - {rz} : 0); k < n0; ++k) {{")
+        a(f"{ind}  int sl = is - n0 + k; while (sl < 0) sl += {s0}; mbar_arrive(empty + sl); }}")
 
 
-def source_block(st: StmtSig, dtype: int, cfg: TbCfg | None = None) -> tuple:
-    """-> (source, kernel name, block, smem, geometry).
-
-    Each compute thread owns RPT points of the step-1 region (W1 x H1, rows
-    interleaved by H1/RPT so warps run along x) for every plane: its own
-    column of every step lives in registers (the pure-z operands), the centre
-    plane of each step is published in shared memory for the neighbours'
-    (dy, dx) operands. Per input plane: one mbarrier wait (TMA), one named
-    barrier, then step 1 .. K each one plane further behind."""
+def source(st: StmtSig, dtype: int, cfg: TbCfg | None = None, py: int = 1056, pz: int = 1056 * 1026,
+           xoff: int = 15) -> tuple:
+    """-> (source, kernel name, block, smem, layout). The buffer pitches (and
+    the padded-box x offset) are compile-time constants so row and plane
+    offsets are immediates; `py`/`pz` default to the C4 layout (1024^3 fp64,
+    depth 1) for prebuilding."""
     cfg = cfg or DEFAULT
     rad = slot_radius(st)[0]
     lay = layout(rad, dtype, cfg)
-    rz, ry, rx = rad
-    K, BX, BY, RPT = cfg.k, cfg.bx, cfg.by, cfg.rpt
-    NT, HG, W1, H1 = lay["nt"], lay["hg"], lay["w1"], lay["h1"]
-    NW = NT // 32
-    T = CTYPE[dtype]
-    q = lay["q"]
-    s0, pl0, w0, h0 = lay["s0"], lay["pl0"], lay["w0"], lay["h0"]
-    E = lay["elem"]
-    L = []
-    a = L.append
-    a(f'// generated by paper_2512_19851_b200/temporal.py — skeleton "tb" (K={K} fused sweeps) {cfg}')
-    a(f"typedef {T} T;")
-    a("struct __align__(64) Tmap { unsigned long long w[16]; };")
-    a("struct __align__(64) Params { Tmap tm;")
-    a("  unsigned long long src, bhome, adst;  // padded-box origins: A now, B (in place), A next")
-    a("  long long py, pz;")
-    a("  int npz, npy, npx, xoff, sz0, sz1, sy0, sy1, sx0, sx1, nbx, nby, zc, nzc, wb; };")
-    L.append(_PTX_HELPERS)
-    a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
-    a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
-    minb = cfg.minb or max(1, min(blocks_per_sm(lay["smem"], NT), 65536 // ((NT + 32) * 96)))
-    lay["min_blocks"] = minb
-    a(f'extern "C" __global__ void __launch_bounds__({NT + 32}, {minb})')
-    a("est_tb(const __grid_constant__ Params p) {")
-    a("  extern __shared__ __align__(1024) unsigned char smem[];")
-    a(f"  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + {lay['data']});")
-    a(f"  unsigned long long* empty = full + {s0};")
-    a("  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;")
-    a("  const int n_items = p.nbx * p.nby * p.nzc;")
-    a("  if (tid == 0) {")
-    a(f"    for (int i = 0; i < {s0}; ++i) {{ mbar_init(full + i, 1); mbar_init(empty + i, {NW}); }}")
-    a(f"    for (int i = 0; i < {(K - 1) * lay['rings'][0]['n'] if K > 1 else 0}; ++i) mbar_init(empty + {s0} + i, {NW});")
-    a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
-    a("  }")
-    a("  __syncthreads();")
-
-    def item_decode(ind):
-        a(f"{ind}const int bx = item % p.nbx, rest = item / p.nbx;")
-        a(f"{ind}const int by = rest % p.nby, bzc = rest / p.nby;")
-        a(f"{ind}const int x0 = p.sx0 + bx * {BX}, y0 = p.sy0 + by * {BY};")
-        a(f"{ind}const int zs = p.sz0 + bzc * p.zc;")
-        a(f"{ind}const int nzl = min(p.zc, p.sz1 - zs);")
-        a(f"{ind}const int n0 = nzl + {2 * K * rz};")
-
-    # ---------------- producer warp
-    a(f"  if (warp == {NW}) {{")
-    a("    if (lane != 0) return;")
-    a("    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm) : \"memory\");")
-    a("    int fill = 0;")
-    a("    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
-    item_decode("      ")
-    a(f"      const int xs = p.xoff + x0 - {K * rx};")
-    a(f"      const int xa = xs - (xs & {q - 1});")
-    a("      for (int k = 0; k < n0; ++k) {")
-    a(f"        const int g = fill + k, stg = g % {s0};")
-    a(f"        if (g >= {s0}) mbar_wait(empty + stg, ((g / {s0}) - 1) & 1);")
-    a(f"        mbar_expect(full + stg, {w0 * h0 * E});")
-    a(f"        tma_load3(smem + stg * {pl0}, &p.tm, xa, y0 - {K * ry}, zs - {K * rz} + k, full + stg);")
-    a("      }")
-    a("      fill += n0;")
-    a("    }")
-    a("    return;")
-    a("  }")
-    # ---------------- compute threads
-    a("  const T* __restrict__ asrc = reinterpret_cast<const T*>(p.src);")
-    a("  T* __restrict__ bmem = reinterpret_cast<T*>(p.bhome);")
-    a("  T* __restrict__ adst = reinterpret_cast<T*>(p.adst);")
-    a(f"  const bool act = tid < {W1 * HG};")
-    a(f"  const int lx = tid % {W1}, lyg = tid / {W1};")
-    # per-row thread constants (item independent)
-    for r in range(RPT):
-        ly = f"(lyg * {RPT} + {r})"
-        a(f"  const int ly{r} = {ly};")
-        for j in range(2, K + 1):
-            lo_y, hi_y = (j - 1) * ry, H1 - (j - 1) * ry
-            lo_x, hi_x = (j - 1) * rx, W1 - (j - 1) * rx
-            a(f"  const bool inT{j}_{r} = act && ly{r} >= {lo_y} && ly{r} < {hi_y} && lx >= {lo_x} && lx < {hi_x};")
-        a(f"  const int so{r} = ly{r} * {W1} + lx;  // step-1 frame smem index")
-        a(f"  const int io{r} = (ly{r} + {ry}) * {w0} + lx + {rx};  // input frame (before the alignment shift)")
-    a("  int fill = 0;")
-    for j in range(1, K):
-        a(f"  unsigned long long* rb{j} = empty + {s0 + (j - 1) * lay['rings'][0]['n']};  // ring {j} slot barriers")
-        a(f"  int f{j} = 0;  // step-{j} planes produced so far (all items)")
-    # register columns: c{j}_{r}_{k} = step-j value (j = 0: input) at the thread point, k = 0..2rz
-    for j in range(0, K):
-        for r in range(RPT):
-            a(f"  T {', '.join(f'c{j}_{r}_{k} = 0' for k in range(2 * rz + 1))};")
-    a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
-    item_decode("    ")
-    a(f"    const int sh = (p.xoff + x0 - {K * rx}) & {q - 1};")
-    for r in range(RPT):
-        a(f"    const int gy{r} = y0 - {(K - 1) * ry} + ly{r}, gx{r} = x0 - {(K - 1) * rx} + lx;")
-        a(f"    const bool sxy{r} = act && gy{r} >= p.sy0 && gy{r} < p.sy1 && gx{r} >= p.sx0 && gx{r} < p.sx1;")
-        a(f"    const bool pxy{r} = act && gy{r} >= 0 && gy{r} < p.npy && gx{r} >= 0 && gx{r} < p.npx;")
-        a(f"    const long long go{r} = (long long)gy{r} * p.py + gx{r};")
-    a(f"    const bool fast = (x0 - {(K - 1) * rx} >= p.sx0) && (x0 + {BX + (K - 1) * rx} <= p.sx1) &&"
-      f" (y0 - {(K - 1) * ry} >= p.sy0) && (y0 + {BY + (K - 1) * ry} <= p.sy1);")
-    a("    if (fast) {")
-    emit_fast_loop(a, st, dtype, lay)
-    a("    } else {")
-    a("    for (int t = 0; t < n0; ++t) {")
-    # prefetch out-of-S values of intermediate steps (home buffers), before any wait
-    for j in range(1, K):
-        home = "bmem" if j % 2 == 1 else "asrc"
-        a(f"      const int z{j} = zs - {(K - j) * rz} + t - {2 * j * rz};")
-        a(f"      const bool zi{j} = z{j} >= p.sz0 && z{j} < p.sz1, zp{j} = z{j} >= 0 && z{j} < p.npz;")
-        for r in range(RPT):
-            inT = "act" if j == 1 else f"inT{j}_{r}"
-            a(f"      T h{j}_{r} = (T)0;")
-            a(f"      if (t >= {2 * j * rz} && {inT} && zp{j} && pxy{r} && !(zi{j} && sxy{r}))"
-              f" h{j}_{r} = {home}[(long long)z{j} * p.pz + go{r}];  // outside S: stored value")
-    a(f"      {{ const int g = fill + t; mbar_wait(full + g % {s0}, (g / {s0}) & 1); }}")
-    a(f"      const T* inC = reinterpret_cast<const T*>(smem) + ((fill + t) % {s0}) * {pl0 // E} + sh;")
-    for r in range(RPT):
-        a(f"      c0_{r}_{2 * rz} = act ? inC[io{r}] : (T)0;")
-    for j in range(1, K + 1):
-        emit_step_b(a, st, dtype, lay, j)
-        if j == 1:
-            a(f"      if (t >= {rz}) {{ __syncwarp(); if (lane == 0) mbar_arrive(empty + (fill + t - {rz}) % {s0}); }}")
-    # rotate the register columns (step j's column only moves once step j ran)
-    for j in range(0, K):
-        cond = "true" if j == 0 else f"t >= {2 * j * rz}"
-        a(f"      if ({cond}) {{")
-        for r in range(RPT):
-            for k in range(2 * rz):
-                a(f"        c{j}_{r}_{k} = c{j}_{r}_{k + 1};")
-        a("      }")
-    a("    }")
-    a("    }  // general path")
-    a(f"    for (int k = (n0 > {rz} ? n0 - {rz} : 0); k < n0; ++k) if (lane == 0) mbar_arrive(empty + (fill + k) % {s0});")
-    a("    fill += n0;")
-    for j in range(1, K):
-        a(f"    f{j} += nzl + {2 * (K - j) * rz};")
-    a("  }")
-    a("}")
-    src = "\n".join(L) + "\n"
-    lay["blocks_per_sm"] = minb
-    return src, "est_tb", (NT + 32, 1, 1), lay["smem"], lay
+    src = _Emitter(st, dtype, lay, py, pz, xoff).source()
+    lay["blocks_per_sm"] = lay["min_blocks"]
+    return src, "est_tb", (lay["nt"] + 32, 1, 1), lay["smem"], lay
 
 
-def source_warp(st: StmtSig, dtype: int, cfg: TbCfg) -> tuple:
-    """K = 2 warp-tiled chain kernel.
-
-    CTA output tile = (30*WX) x (R*WY) columns x rows, streamed along z; the
-    producer warp TMA-loads each input plane (tile + 2-cell halo) into an
-    mbarrier ring. Each compute warp owns 30 output columns x R rows: lane l
-    holds column l-1, so lanes 0 and 31 carry the x-halo of the intermediate
-    sweep. Step 1 (B at t+1) is computed for rows -1..R of the warp from the
-    shared input plane (z-neighbours from a per-lane register window); step 2
-    (A at t+2) reads step 1 only from registers: own rows / y-neighbours
-    directly, x-neighbours through warp shuffles. No shared memory for the
-    intermediate sweep and no barrier between warps."""
-    rz, ry, rx = slot_radius(st)[0]
-    T = CTYPE[dtype]
-    elem = ELEM[dtype]
-    q = 16 // elem
-    WX, WY, R = cfg.wx, cfg.wy, cfg.r
-    BX, BY = 30 * WX, R * WY
-    NW = WX * WY
-    NT = 32 * NW
-    w0 = _round(BX + 4 + q - 1, q)
-    h0 = BY + 4
-    s0 = 2 + cfg.prefetch
-    pl0 = _round(w0 * h0 * elem, 1024)
-    data = s0 * pl0
-    smem = data + 8 * 2 * s0 + 1024
-    minb = cfg.minb or max(1, min(SMEM_PER_SM // (smem + 1024), 65536 // ((NT + 32) * 96), 2048 // (NT + 32)))
-    lay = {"rad": (rz, ry, rx), "w0": w0, "h0": h0, "s0": s0, "pl0": pl0, "data": data, "smem": smem,
-           "cfg": cfg, "elem": elem, "q": q, "bx": BX, "by": BY, "nt": NT, "min_blocks": minb,
-           "blocks_per_sm": minb, "variant": "warp"}
-    ROWS = list(range(-1, R + 1))          # step-1 rows of a warp (rr = r + 1)
-    L = []
-    a = L.append
-    a(f'// generated by paper_2512_19851_b200/temporal.py — skeleton "tb" warp-tiled (K=2) {cfg}')
-    a(f"typedef {T} T;")
-    a("struct __align__(64) Tmap { unsigned long long w[16]; };")
-    a("struct __align__(64) Params { Tmap tm;")
-    a("  unsigned long long src, bhome, adst;  // padded-box origins: A now, B (in place), A next")
-    a("  long long py, pz;")
-    a("  int npz, npy, npx, xoff, sz0, sz1, sy0, sy1, sx0, sx1, nbx, nby, zc, nzc, wb; };")
-    L.append(_PTX_HELPERS)
-    a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
-    a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
-    a(f'extern "C" __global__ void __launch_bounds__({NT + 32}, {minb})')
-    a("est_tb(const __grid_constant__ Params p) {")
-    a("  extern __shared__ __align__(1024) unsigned char smem[];")
-    a(f"  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + {data});")
-    a(f"  unsigned long long* empty = full + {s0};")
-    a("  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;")
-    a("  const int n_items = p.nbx * p.nby * p.nzc;")
-    a("  if (tid == 0) {")
-    a(f"    for (int i = 0; i < {s0}; ++i) {{ mbar_init(full + i, 1); mbar_init(empty + i, {NW}); }}")
-    a("    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");")
-    a("  }")
-    a("  __syncthreads();")
-
-    def item_decode(ind):
-        a(f"{ind}const int bx = item % p.nbx, rest = item / p.nbx;")
-        a(f"{ind}const int by = rest % p.nby, bzc = rest / p.nby;")
-        a(f"{ind}const int x0 = p.sx0 + bx * {BX}, y0 = p.sy0 + by * {BY};")
-        a(f"{ind}const int zs = p.sz0 + bzc * p.zc;")
-        a(f"{ind}const int nzl = min(p.zc, p.sz1 - zs);")
-        a(f"{ind}const int n0 = nzl + 4;")
-
-    # ---------------- producer warp
-    a(f"  if (warp == {NW}) {{")
-    a("    if (lane != 0) return;")
-    a("    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tm) : \"memory\");")
-    a("    int fill = 0;")
-    a("    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
-    item_decode("      ")
-    a("      const int xs = p.xoff + x0 - 2;")
-    a(f"      const int xa = xs - (xs & {q - 1});")
-    a("      for (int k = 0; k < n0; ++k) {")
-    a(f"        const int g = fill + k, stg = g % {s0};")
-    a(f"        if (g >= {s0}) mbar_wait(empty + stg, ((g / {s0}) - 1) & 1);")
-    a(f"        mbar_expect(full + stg, {w0 * h0 * elem});")
-    a(f"        tma_load3(smem + stg * {pl0}, &p.tm, xa, y0 - 2, zs - 2 + k, full + stg);")
-    a("      }")
-    a("      fill += n0;")
-    a("    }")
-    a("    return;")
-    a("  }")
-    # ---------------- compute warps
-    a("  const T* __restrict__ asrc = reinterpret_cast<const T*>(p.src); (void)asrc;")
-    a("  T* __restrict__ bmem = reinterpret_cast<T*>(p.bhome);")
-    a("  T* __restrict__ adst = reinterpret_cast<T*>(p.adst);")
-    a(f"  const int wxi = warp % {WX}, wyi = warp / {WX};")
-    a("  const bool own = lane >= 1 && lane <= 30;")
-    a("  const long long py = p.py, pz = p.pz;")
-    a("  int fill = 0;")
-    for j in (0, 1):
-        for rr in range(len(ROWS)):
-            a(f"  T {', '.join(f'c{j}_{rr}_{k} = 0' for k in range(3))};")
-    a("  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {")
-    item_decode("    ")
-    a(f"    const int sh = (p.xoff + x0 - 2) & {q - 1};")
-    a(f"    const int scol = sh + 30 * wxi + lane + 1;   // smem column of this lane (output column lane-1)")
-    a(f"    const int srow = {R} * wyi + 2;               // smem row of warp row 0")
-    a("    const int gx = x0 + 30 * wxi + lane - 1;")
-    a("    const bool colS = gx >= p.sx0 && gx < p.sx1, colP = gx >= 0 && gx < p.npx;")
-    a(f"    const int gy0 = y0 + {R} * wyi;")
-    for rr, r in enumerate(ROWS):
-        a(f"    const bool rS{rr} = (gy0 + {r}) >= p.sy0 && (gy0 + {r}) < p.sy1 && colS;")
-        a(f"    const bool rP{rr} = (gy0 + {r}) >= 0 && (gy0 + {r}) < p.npy && colP;")
-    a("    const long long cb = (long long)gy0 * py + gx;  // row-0 offset of this lane within a plane")
-    a("    const T* ring = reinterpret_cast<const T*>(smem) + sh * 0;")
-    a(f"    for (int t0 = 0; t0 < n0; t0 += 3) {{")
-    for m in range(3):
-        def col(j, rr, k, m=m):
-            return f"c{j}_{rr}_{(k + m) % 3}"
-        a(f"      if (t0 + {m} < n0) {{")
-        a(f"      const int t = t0 + {m};")
-        a(f"      {{ const int g = fill + t; mbar_wait(full + g % {s0}, (g / {s0}) & 1); }}")
-        a(f"      const T* Pn = ring + ((fill + t) % {s0}) * {pl0 // elem} + srow * {w0} + scol;  // input plane t")
-        for rr, r in enumerate(ROWS):
-            a(f"      {col(0, rr, 2)} = Pn[{r * w0}];")
-        # ---- step 1: plane index t-1 of the input is the centre plane
-        a("      if (t >= 2) {")
-        a(f"        const T* Pc = ring + ((fill + t - 1) % {s0}) * {pl0 // elem} + srow * {w0} + scol;")
-        a("        const int z1 = zs - 1 + (t - 2);")
-        a("        const bool zin1 = z1 >= p.sz0 && z1 < p.sz1, zp1 = z1 >= 0 && z1 < p.npz;")
-        a("        const long long zo1 = (long long)z1 * pz + cb;")
-        for rr, r in enumerate(ROWS):
-            def load1(slot, off3, rr=rr, r=r):
-                dz, dy, dx = off3
-                if dz != 0 or (dy == 0 and dx == 0):
-                    return col(0, rr, 1 + dz)
-                if dx == 0 and 0 <= rr + dy < len(ROWS):
-                    return col(0, rr + dy, 1)
-                return f"Pc[{(r + dy) * w0 + dx}]"
-            lines, res = _emit_expr(st, dtype, load1)
-            a(f"        {{ T v;")
-            a(f"          if (zin1 && rS{rr}) {{")
-            for ln in lines:
-                a(f"            {ln}")
-            a(f"            v = {res};")
-            if 0 <= r < R:
-                a(f"            if (own && p.wb) bmem[zo1 + {r} * py] = v;")
-            a(f"          }} else {{")
-            a(f"            v = (zp1 && rP{rr}) ? bmem[zo1 + {r} * py] : ({T})0;  // outside S: stored value")
-            a("          }")
-            a(f"          {col(1, rr, 2)} = v; }}")
-        a("      }")
-        a(f"      if (t >= 1) {{ __syncwarp(); if (lane == 0) mbar_arrive(empty + (fill + t - 1) % {s0}); }}")
-        # ---- step 2: step-1 index t-3 is the centre
-        a("      if (t >= 4) {")
-        a("        const int z2 = zs + (t - 4);")
-        a("        const bool zin2 = z2 >= p.sz0 && z2 < p.sz1;")
-        a("        const long long zo2 = (long long)z2 * pz + cb;")
-        # shuffled neighbours needed
-        need = set()
-        for i in st.instructions:
-            if i[0] == "load" and i[2][0] == 0 and i[2][2] != 0:
-                need.add((i[2][1], i[2][2]))
-        shf = {}
-        for r in range(R):
-            rr = r + 1
-            for dy, dx in sorted(need):
-                key = (rr + dy, dx)
-                if key not in shf:
-                    nm = f"sf{rr + dy}_{'m' if dx < 0 else 'p'}{abs(dx)}"
-                    shf[key] = nm
-                    a(f"        const T {nm} = __shfl_sync(0xffffffffu, {col(1, rr + dy, 1)}, (lane + ({dx})) & 31);")
-        for r in range(R):
-            rr = r + 1
-            def load2(slot, off3, rr=rr):
-                dz, dy, dx = off3
-                if dz != 0 or (dy == 0 and dx == 0):
-                    return col(1, rr, 1 + dz)
-                if dx == 0:
-                    return col(1, rr + dy, 1)
-                return shf[(rr + dy, dx)]
-            lines, res = _emit_expr(st, dtype, load2)
-            a(f"        if (zin2 && rS{rr} && own) {{")
-            for ln in lines:
-                a(f"          {ln}")
-            a(f"          adst[zo2 + {r} * py] = {res};")
-            a("        }")
-        a("      }")
-        a("      }")
-    a("    }")
-    a(f"    if (lane == 0) mbar_arrive(empty + (fill + n0 - 1) % {s0});")
-    a("    fill += n0;")
-    a("  }")
-    a("}")
-    src = "\n".join(L) + "\n"
-    return src, "est_tb", (NT + 32, 1, 1), smem, lay
-
-
-def emit_fast_loop(a, st: StmtSig, dtype: int, lay: dict) -> None:
-    """Items whose whole step-1 region lies inside S in y/x: no per-point
-    S tests (planes outside S's z range take a uniform branch), store
-    pointers advanced per plane, ring slots as counters, and the plane loop
-    unrolled 2rz+1 times so the register columns rotate by renaming."""
+def item_geometry(s_lo, s_hi, sm_count: int, lay: dict, xoff: int = 0) -> dict:
+    """Work-item tiling of the output box S (padded coordinates): x tiles
+    start at the vector-aligned column at or below S's first column, z chunks
+    are balanced (every item has the same number of planes but the last)."""
     cfg = lay["cfg"]
-    K, RPT = cfg.k, cfg.rpt
-    rz, ry, rx = lay["rad"]
-    s0, E = lay["s0"], lay["elem"]
-    pl0, pl1 = lay["pl0"] // E, lay["pl1"] // E
-    Z = 2 * rz + 1          # register column length = unroll factor
-    ind = "      "
-    a(f"{ind}const long long pz = p.pz;")
-    for r in range(RPT):
-        a(f"{ind}T* bp{r} = bmem + (long long)(zs - {rz}) * pz + go{r};  // step K-1 (B) plane 0")
-        a(f"{ind}T* ap{r} = adst + (long long)zs * pz + go{r};  // step K (A next) plane 0")
-    a(f"{ind}int is = fill % {s0}, ip = (fill / {s0}) & 1;  // input slot / phase of index t")
-    a(f"{ind}const T* ring0 = reinterpret_cast<const T*>(smem) + sh;")
-    a(f"{ind}for (int t0 = 0; t0 < n0; t0 += {Z}) {{")
-    for m in range(Z):
-        # logical column index k (0 = oldest of the window) lives in name (k + m) % Z
-        def col(j, r, k, m=m):
-            return f"c{j}_{r}_{(k + m) % Z}"
-        a(f"{ind}  if (t0 + {m} < n0) {{  // plane iteration t = t0 + {m}")
-        a(f"{ind}  const int t = t0 + {m};")
-        a(f"{ind}  mbar_wait(full + is, ip);")
-        a(f"{ind}  {{ const T* inC = ring0 + is * {pl0};")
-        for r in range(RPT):
-            a(f"{ind}    {col(0, r, 2 * rz)} = inC[io{r}];")
-        a(f"{ind}  }}")
-        a(f"{ind}  int ir = is - {rz}; if (ir < 0) ir += {s0};  // slot of index t - rz")
-        for j in range(1, K + 1):
-            final = j == K
-            a(f"{ind}  if (t >= {2 * j * rz}) {{  // step {j}")
-            a(f"{ind}    const bool zin = (zs - {(K - j) * rz} + t - {2 * j * rz}) >= p.sz0 &&"
-              f" (zs - {(K - j) * rz} + t - {2 * j * rz}) < p.sz1;")
-            if j == 1:
-                a(f"{ind}    const T* P = ring0 + ir * {pl0};")
-            else:
-                rp = lay["rings"][j - 2]
-                nr = rp["n"]
-                a(f"{ind}    const int gr = f{j - 1} + t - {(2 * j - 1) * rz};")
-                a(f"{ind}    mbar_wait(rb{j - 1} + gr % {nr}, (gr / {nr}) & 1);")
-                a(f"{ind}    const T* P = reinterpret_cast<const T*>(smem + {rp['off']}) + (gr % {nr}) * {pl1};")
-            if not final:
-                rg = lay["rings"][j - 1]
-                a(f"{ind}    const int gw = f{j} + t - {2 * j * rz};")
-                a(f"{ind}    T* Wr = reinterpret_cast<T*>(smem + {rg['off']}) + (gw % {rg['n']}) * {pl1};")
-                home = "bmem" if j % 2 == 1 else "asrc"
-                a(f"{ind}    const long long zo = (long long)(zs - {(K - j) * rz} + t - {2 * j * rz}) * pz;")
-            a(f"{ind}    if (zin) {{")
-            for r in range(RPT):
-                inT = "act" if j == 1 else f"inT{j}_{r}"
-                base = f"io{r}" if j == 1 else f"so{r}"
-                pitch = lay["w0"] if j == 1 else lay["w1"]
-
-                def load(slot, off3, r=r, base=base, pitch=pitch, j=j):
-                    dz, dy, dx = off3
-                    if dz != 0 or (dy == 0 and dx == 0):
-                        return col(j - 1, r, rz + dz)
-                    if dx == 0 and 0 <= r + dy < RPT:
-                        return col(j - 1, r + dy, rz)
-                    return f"P[{base} + {dy * pitch + dx}]"
-
-                lines, res = _emit_expr(st, dtype, load)
-                a(f"{ind}      if ({inT}) {{")
-                for ln in lines:
-                    a(f"{ind}        {ln}")
-                if final:
-                    a(f"{ind}        *ap{r} = {res};")
-                else:
-                    a(f"{ind}        Wr[so{r}] = {res};")
-                    a(f"{ind}        {col(j, r, 2 * rz)} = {res};")
-                    if j == K - 1:
-                        a(f"{ind}        if (p.wb && inT{K}_{r}) *bp{r} = {res};")
-                a(f"{ind}      }}")
-            a(f"{ind}    }}")
-            if not final:
-                a(f"{ind}    else {{  // plane outside S: the array's stored value (0 beyond the padded box,")
-                a(f"{ind}           // which deeper chains reach at the first and last planes)")
-                a(f"{ind}      const int zq = zs - {(K - j) * rz} + t - {2 * j * rz};")
-                a(f"{ind}      const bool zp = zq >= 0 && zq < p.npz;")
-                for r in range(RPT):
-                    inT = "act" if j == 1 else f"inT{j}_{r}"
-                    a(f"{ind}      if ({inT}) {{ const T v = zp ? {home}[zo + go{r}] : (T)0; Wr[so{r}] = v;"
-                      f" {col(j, r, 2 * rz)} = v; }}")
-                a(f"{ind}    }}")
-            for r in range(RPT):
-                if final:
-                    a(f"{ind}    ap{r} += pz;")
-                elif j == K - 1:
-                    a(f"{ind}    bp{r} += pz;")
-            if not final:
-                a(f"{ind}    __syncwarp(); if (lane == 0) mbar_arrive(rb{j} + gw % {lay['rings'][j - 1]['n']});")
-            a(f"{ind}  }}")
-            if j == 1:
-                a(f"{ind}  if (t >= {rz}) {{ __syncwarp(); if (lane == 0) mbar_arrive(empty + ir); }}")
-        a(f"{ind}  if (++is == {s0}) {{ is = 0; ip ^= 1; }}")
-        a(f"{ind}  }}")
-    a(f"{ind}}}")
-
-
-def emit_step_b(a, st: StmtSig, dtype: int, lay: dict, j: int) -> None:
-    """Step j at input iteration t: index u = t - 2*j*rz, centre plane of the
-    previous step at index u + rz (input ring for j = 1, ring j-1 otherwise)."""
-    cfg = lay["cfg"]
-    K, RPT = cfg.k, cfg.rpt
-    rz, ry, rx = lay["rad"]
-    W1 = lay["w1"]
-    E = lay["elem"]
-    final = j == K
-    ind = "        "
-    a(f"      if (t >= {2 * j * rz}) {{  // step {j}")
-    a(f"{ind}const int u = t - {2 * j * rz};")
-    a(f"{ind}const int zj = zs - {(K - j) * rz} + u;")
-    a(f"{ind}const bool zin = zj >= p.sz0 && zj < p.sz1;")
-    a(f"{ind}const long long zoff = (long long)zj * p.pz;")
-    if j == 1:
-        a(f"{ind}const T* P = reinterpret_cast<const T*>(smem) + ((fill + t - {rz}) % {lay['s0']}) * {lay['pl0'] // E} + sh;")
-    else:
-        rp = lay["rings"][j - 2]
-        nr = rp["n"]
-        a(f"{ind}const int gr = f{j - 1} + t - {(2 * j - 1) * rz};  // step-{j - 1} plane read")
-        a(f"{ind}mbar_wait(rb{j - 1} + gr % {nr}, (gr / {nr}) & 1);")
-        a(f"{ind}const T* P = reinterpret_cast<const T*>(smem + {rp['off']}) + (gr % {nr}) * {lay['pl1'] // E};")
-    if not final:
-        rg = lay["rings"][j - 1]
-        a(f"{ind}const int gw = f{j} + u;")
-        a(f"{ind}T* W = reinterpret_cast<T*>(smem + {rg['off']}) + (gw % {rg['n']}) * {lay['pl1'] // E};")
-    for r in range(RPT):
-        inT = "act" if j == 1 else f"inT{j}_{r}"
-        base = f"io{r}" if j == 1 else f"so{r}"
-        pitch = lay["w0"] if j == 1 else W1
-
-        def load(slot, off3, r=r, base=base, pitch=pitch):
-            dz, dy, dx = off3
-            if dz != 0 or (dy == 0 and dx == 0):
-                return f"c{j - 1}_{r}_{rz + dz}"
-            if dx == 0 and 0 <= r + dy < RPT:
-                return f"c{j - 1}_{r + dy}_{rz}"  # the thread's own neighbouring row
-            return f"P[{base} + {dy * pitch + dx}]"
-
-        lines, res = _emit_expr(st, dtype, load)
-        a(f"{ind}if ({inT}) {{")
-        a(f"{ind}  T v;")
-        a(f"{ind}  if (zin && sxy{r}) {{")
-        for ln in lines:
-            a(f"{ind}    {ln}")
-        a(f"{ind}    v = {res};")
-        if final:
-            a(f"{ind}    adst[zoff + go{r}] = v;")
-        elif j == K - 1:
-            a(f"{ind}    if (p.wb && inT{K}_{r}) bmem[zoff + go{r}] = v;")
-        a(f"{ind}  }} else {{")
-        a(f"{ind}    v = {'(T)0' if final else f'h{j}_{r}'};")
-        a(f"{ind}  }}")
-        if not final:
-            a(f"{ind}  W[so{r}] = v;")
-            a(f"{ind}  c{j}_{r}_{2 * rz} = v;")
-        a(f"{ind}}}")
-    if not final:
-        a(f"{ind}__syncwarp(); if (lane == 0) mbar_arrive(rb{j} + gw % {lay['rings'][j - 1]['n']});")
-    a("      }")
-
-
-def item_geometry(s_lo, s_hi, sm_count: int, lay: dict) -> dict:
-    """Work-item tiling of the output box S (padded coordinates)."""
-    cfg = lay["cfg"]
-    nz, ny, nx = (b - a for a, b in zip(s_lo, s_hi))
-    nbx, nby = -(-nx // lay.get("bx", cfg.bx)), -(-ny // lay.get("by", cfg.by))
-    zc = min(cfg.zchunk, nz)
+    V = lay["V"]
+    nz, ny = s_hi[0] - s_lo[0], s_hi[1] - s_lo[1]
+    xt0 = s_lo[2] - ((xoff + s_lo[2]) % V)
+    nbx = -(-(s_hi[2] - xt0) // cfg.bx)
+    nby = -(-ny // cfg.by)
+    nzc = max(1, -(-nz // max(1, cfg.zchunk)))
+    zc = -(-nz // nzc)
     nzc = -(-nz // zc)
     n_items = nbx * nby * nzc
     cap = sm_count * lay.get("min_blocks", 1)
     blocks = min(n_items, cap) if cfg.persistent else n_items
-    return {"nbx": nbx, "nby": nby, "zc": zc, "nzc": nzc, "blocks": blocks}
+    return {"nbx": nbx, "nby": nby, "zc": zc, "nzc": nzc, "blocks": blocks, "xt0": xt0}
 
 
 def pack_params(tmap: bytes, src: int, bhome: int, adst: int, buf, s_lo, s_hi, geo: dict,
@@ -688,9 +498,9 @@ def pack_params(tmap: bytes, src: int, bhome: int, adst: int, buf, s_lo, s_hi, g
     assert len(tmap) == 128
     npz, npy, npx = buf.nz, buf.pz // buf.py, buf.ext[2] + 2 * buf.depth[2]
     out = bytearray(tmap)
-    out += struct.pack("<QQQqq", src, bhome, adst, buf.py, buf.pz)
-    out += struct.pack("<15i", npz, npy, npx, buf.xoff, s_lo[0], s_hi[0], s_lo[1], s_hi[1],
-                       s_lo[2], s_hi[2], geo["nbx"], geo["nby"], geo["zc"], geo["nzc"], int(write_b))
+    out += struct.pack("<QQQ", src, bhome, adst)
+    out += struct.pack("<15i", npz, npy, npx, s_lo[0], s_hi[0], s_lo[1], s_hi[1],
+                       s_lo[2], s_hi[2], geo["xt0"], geo["nbx"], geo["nby"], geo["zc"], geo["nzc"], int(write_b))
     return bytes(out) + b"\0" * ((-len(out)) % 64)
 
 

@@ -141,6 +141,16 @@ class TileBuffer:
         self.serial = next(TileBuffer._serials)  # identifies this allocation in peer tables
 
     @staticmethod
+    def pitches(ext, depth, dtype: int) -> tuple:
+        """(xoff, py, pz) in elements of a buffer with this extent / depth."""
+        elem = np.dtype(NP_DTYPE[dtype]).itemsize
+        align = ALIGN_BYTES // elem
+        e, d = pad3(ext, 1), pad3(depth, 0)
+        xoff = (align - d[2] % align) % align
+        py = -(-(xoff + e[2] + 2 * d[2]) // align) * align
+        return xoff, py, py * (e[1] + 2 * d[1])
+
+    @staticmethod
     def layout_bytes(ext, depth, dtype: int) -> int:
         elem = np.dtype(NP_DTYPE[dtype]).itemsize
         align = ALIGN_BYTES // elem
@@ -362,21 +372,35 @@ class GpuTileStore:
         return header + np.ascontiguousarray(block).astype(block.dtype.newbyteorder("<"), copy=False).tobytes()
 
     def adopt_blob(self, blob: bytes) -> tuple:
-        """adopt_blob (grid.py:264-277): install a checkpointed interior into
-        the owned tile (ghost frame grown to the blob's depth if needed and
-        zeroed), epochs from the blob. -> (array, coords, epoch)."""
+        """adopt_blob (grid.py:264-277): install a checkpointed tile payload.
+
+        As in the reference the tile is created if this worker does not own it
+        yet (`tiles.setdefault`), its buffer is (re)allocated zeroed at the
+        BLOB's ghost depth, and the tile's epochs come from the blob; the
+        store-level epoch counters follow (every blob of one checkpoint carries
+        the same epoch; the adopting path bumps them uniformly afterwards).
+        -> (array, coords, epoch)."""
         array, coords, ext, depth, epoch, hs = parse_blob_header(blob)
         info = self.arrays[array]
         if tuple(ext) != tuple(self.decomp.tile_extents(info.shape)):
             raise InvalidShape(f"blob extent {ext} does not match array {array}'s tiles")
-        self.ensure_ghost_capacity(array, depth)
-        buf = self.tiles[coords].buffers[array]
+        self.check_depth_fits(array, depth)
+        coords = tuple(coords)
+        tile = self.tiles.setdefault(coords, GpuTile(coords))
+        old = tile.buffers.get(array)
+        if old is None or tuple(old.depth[3 - old.rank:]) != tuple(depth):
+            if old is not None:
+                old.free()
+            tile.buffers[array] = TileBuffer(self.dev, ext, depth, info.dtype)
+            self.version += 1
+        buf = tile.buffers[array]
         self.dev.memset_zero(buf.ptr, buf.nbytes, COMPUTE)
+        tile.depths[array] = tuple(depth)
         data = np.frombuffer(blob, dtype=np.dtype(NP_DTYPE[info.dtype]).newbyteorder("<"),
                              offset=hs).reshape(ext)
         self.upload_interior(coords, array, data)
-        tile = self.tiles[coords]
         tile.local_epoch[array] = tile.ghost_epoch[array] = epoch
+        self._epochs[array] = self._ghosts[array] = epoch
         return array, coords, epoch
 
     def release(self) -> None:

@@ -97,7 +97,7 @@ class FakeDevice:
     def occupancy(self, k):
         return 8
 
-    def launch(self, k, grid, params, stream=0, pdl=True):
+    def launch(self, k, grid, params, stream=0, pdl=True, cooperative=False):
         self.launches += 1
         self.log.append(("launch", grid[0], getattr(k, "name", "")))
         self.params.append(params)

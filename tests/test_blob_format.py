@@ -57,7 +57,16 @@ def test_gpu_export_and_adopt_round_trip():
             np.testing.assert_array_equal(dst.fetch(case), src.fetch(case))
             for g in blobs:
                 assert dst.checkpoint_blob(tuple(g["coords"]), case) == bytes.fromhex(g["blob"])
+            # a worker that owns none of the tiles adopts them (grid.py:271 setdefault)
+            # at the blob's depth, with the blob's epochs
+            empty = GpuTileStore(dev, decomp, [])
+            empty.create_array(ArrayInfo(case, shape))
+            for g in blobs:
+                empty.adopt_blob(bytes.fromhex(g["blob"]))
+                assert empty.checkpoint_blob(tuple(g["coords"]), case) == bytes.fromhex(g["blob"])
+            assert empty.local_epoch(case) == g0["epoch"] and len(empty.tiles) == len(blobs)
             src.release()
             dst.release()
+            empty.release()
     finally:
         dev.close()

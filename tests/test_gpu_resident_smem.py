@@ -24,11 +24,9 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def only_rsm(monkeypatch):
-    from paper_2512_19851_b200 import resident, temporal, wavefront
+    from paper_2512_19851_b200 import resident, temporal
     monkeypatch.setattr(resident, "SMEM_ENABLED", True)
-    monkeypatch.setattr(resident, "ENABLED", False)
     monkeypatch.setattr(temporal, "ENABLED", False)
-    monkeypatch.setattr(wavefront, "ENABLED", False)
 
 
 def _ran(job) -> bool:

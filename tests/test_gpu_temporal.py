@@ -1,8 +1,8 @@
-"""GPU parity of the fused-chain skeletons: temporal.py (K fused ping-pong
-sweeps with a twin buffer) and resident.py (a whole L2-resident run in one
-persistent launch with grid barriers). Both must be bit-identical to the
-oracle (fp64; fp32 within the north star's 1e-5, in fact bit-identical
-because the plan order is kept). Every test runs in both modes.
+"""GPU parity of the fused-chain skeleton temporal.py (K fused ping-pong
+sweeps with a twin buffer): bit-identical to the oracle (fp64; fp32 within the
+north star's 1e-5, in fact bit-identical because the plan order is kept).
+Every test runs with the default K = 2 chain and with a K = 4 chain (smaller
+tiles so its three intermediate plane rings fit shared memory).
 
 Cases cover partial tiles, output slices that are not the full interior, a
 radius-2 and an asymmetric stencil, odd iteration counts (a leftover sweep on
@@ -20,25 +20,29 @@ from paper_2512_19851_b200.wire import DTYPE_F32, encode_dag
 
 pytestmark = pytest.mark.gpu
 
+K4 = dict(k=4, bx=32, by=32)
 
-@pytest.fixture(autouse=True, params=["tb", "tb-warp", "resident", "wave"])
+
+@pytest.fixture(autouse=True, params=["k2", "k4"])
 def mode(request, monkeypatch):
     import dataclasses
 
-    from paper_2512_19851_b200 import resident, temporal, wavefront
-    monkeypatch.setattr(temporal, "ENABLED", request.param.startswith("tb"))
-    monkeypatch.setattr(resident, "ENABLED", request.param == "resident")
-    monkeypatch.setattr(wavefront, "ENABLED", request.param == "wave")
+    from paper_2512_19851_b200 import resident, temporal
+    monkeypatch.setattr(temporal, "ENABLED", True)
     monkeypatch.setattr(resident, "SMEM_ENABLED", False)  # tests/test_gpu_resident_smem.py
     monkeypatch.setattr(temporal, "MIN_POINTS", 0)  # chains at test sizes
-    if request.param == "tb-warp":
-        monkeypatch.setattr(temporal, "DEFAULT", dataclasses.replace(temporal.DEFAULT, variant="warp"))
-    return "tb" if request.param.startswith("tb") else request.param
+    if request.param == "k4":
+        monkeypatch.setattr(temporal, "DEFAULT", dataclasses.replace(temporal.DEFAULT, **K4))
+    return request.param
 
 
 def _ran(job, mode) -> bool:
-    ex = job.executors[0]
-    return {"tb": bool(ex._scratch), "resident": bool(ex._bar), "wave": bool(ex._wave_ctr[0])}[mode]
+    return bool(job.executors[0]._scratch)
+
+
+def _chains(mode, sweeps: int) -> bool:
+    """A run of `sweeps` ping-pong nodes holds an even number (>= 2) of K-chains."""
+    return sweeps >= 2 * (4 if mode == "k4" else 2)
 
 
 def _tb_launches(stats) -> int:
@@ -52,7 +56,7 @@ def test_heat3d_chains_bit_exact(n, iters, mode):
     want = strict_execute_dag(prog.dag, prog.shapes)
     job, stats = run_program(prog, fused=True)
     try:
-        assert _ran(job, mode), "fused chain did not run"
+        assert _ran(job, mode) == _chains(mode, iters), "fused chain did not run"
         for aid in prog.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), (n, iters, aid)
     finally:
@@ -104,7 +108,7 @@ def test_asymmetric_offsets_bit_exact(mode):
 
     def at(u, dz, dy, dx):
         return ref(u, tuple(slice(lo + d, hi + d) for (lo, hi), d in zip(box, (dz, dy, dx))))
-    for _ in range(6):
+    for _ in range(8):
         e = add(mul(cst(0.5), at(u1, -2, 0, 0)), mul(cst(0.25), at(u1, 0, 1, -1)))
         e = sub(e, mul(cst(0.125), at(u1, 1, 0, 0)))
         e = add(e, at(u1, 0, -1, 0))
@@ -161,9 +165,9 @@ def test_repeated_batches_graph_replay_bit_exact(mode):
         job.run(setup.dag)
         stats = [job.run_bytes(blob) for _ in range(batches)]
         assert job.executors[0].replays >= 2
-        # tb: 10 sweeps = 4 chains of 2 (chain count kept even) + 2 single sweeps
-        # + the complement copy; resident: the whole batch is one launch
-        assert stats[1][0].gpu_launches == {"tb": 4 + 2 + 1, "resident": 1, "wave": 5}[mode]
+        # 10 sweeps = 4 chains of 2 (K = 2; chain count kept even) or 2 chains of 4
+        # + 2 single sweeps + the complement copy
+        assert stats[1][0].gpu_launches == {"k2": 4 + 2 + 1, "k4": 2 + 2 + 1}[mode]
         for aid in setup.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), aid
 
@@ -178,9 +182,7 @@ def test_chain_disabled_equals_enabled(mode):
         try:
             for aid in sorted(prog.shapes):
                 job.create_array(prog.shapes[aid])
-            job.executors[0].temporal = on and mode == "tb"
-            job.executors[0].resident = on and mode == "resident"
-            job.executors[0].wave = on and mode == "wave"
+            job.executors[0].temporal = on
             job_stats = job.run(prog.dag)
             outs.append([job.fetch(a) for a in sorted(prog.shapes)])
             assert _ran(job, mode) == on
@@ -192,8 +194,7 @@ def test_chain_disabled_equals_enabled(mode):
 
 
 def test_non_z_star_chain(mode):
-    """A diagonal (dz, dx) load: not chainable by tb (no twin), resident runs
-    it; bit-exact either way."""
+    """A diagonal (dz, dx) load is not chainable (z-star only): node by node, bit-exact."""
     n = 32
     prog = DagProgram()
     u1, u2 = heat3d_setup(prog, n, seed_fills=6)
@@ -207,28 +208,16 @@ def test_non_z_star_chain(mode):
     want = reference_execute_dag(prog.dag, prog.shapes)
     job, _ = run_program(prog)
     try:
-        assert _ran(job, mode) == (mode in ("resident", "wave"))
+        assert not _ran(job, mode)
         for aid in prog.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), aid
     finally:
         job.close()
 
 
-def test_resident_2d_laplace_and_wave_sizes(mode):
-    """2-D runs: Laplace 1024^2 x 100 (BASELINE C1) in one launch; the fp32 wave
-    (three rotating arrays) is not a ping-pong chain and stays node by node."""
-    if mode != "resident":
-        pytest.skip("2-D chains are resident-only")
-    from oracle.oracle import laplace_reference
-    from paper_2512_19851_b200.programs import laplace_program, wave2d_program
-    prog = DagProgram()
-    names = laplace_program(prog, 1024, 100)
-    job, stats = run_program(prog, fused=True)
-    try:
-        assert _ran(job, mode)
-        assert bits_equal(job.fetch(names["u"]), laplace_reference(1024, 100))
-    finally:
-        job.close()
+def test_wave_is_not_a_chain(mode):
+    """The fp32 wave (three rotating arrays) is not a ping-pong chain: node by node."""
+    from paper_2512_19851_b200.programs import wave2d_program
     prog = DagProgram()
     names = wave2d_program(prog, 128, 12, dtype=DTYPE_F32)
     want = reference_execute_dag(prog.dag, prog.shapes, prog.dtypes)
@@ -241,15 +230,13 @@ def test_resident_2d_laplace_and_wave_sizes(mode):
 
 
 def test_default_chain_at_full_scheduling_size(mode, monkeypatch):
-    """The default path (tb from 2^28 output points) at a size where it is
-    actually scheduled: 648^3 (646^3 = 269.6 M outputs), 4 iterations = 2
+    """The default path (tb from MIN_POINTS output points) at a size where it is
+    actually scheduled: 648^3 (646^3 = 269.6 M outputs), 8 iterations = 4 / 2
     chains, seeded fills; every array bit-identical to the strict oracle."""
-    if mode != "tb":
-        pytest.skip("the size threshold only gates tb")
     from paper_2512_19851_b200 import temporal
-    monkeypatch.setattr(temporal, "MIN_POINTS", 1 << 28)
+    monkeypatch.setattr(temporal, "MIN_POINTS", int(temporal.os.environ.get("EST_TB_MIN_POINTS", 1 << 26)))
     prog = DagProgram()
-    heat3d_program(prog, 648, 4, seed_fills=12)
+    heat3d_program(prog, 648, 8, seed_fills=12)
     want = strict_execute_dag(prog.dag, prog.shapes)
     job, _ = run_program(prog)
     try:
@@ -265,8 +252,6 @@ def test_random_z_star_chains(seed, mode):
     """Random 3-D ping-pong chains the tb skeleton accepts (in-plane offsets
     of radius <= 2 in y/x, pure z offsets of radius 1-2, any signs), random
     boxes, constants, dtypes and even sweep counts."""
-    if mode != "tb":
-        pytest.skip("tb-specific shapes")
     import random as _r
     rng = _r.Random(7700 + seed)
     n = (rng.randrange(12, 60), rng.randrange(12, 90), rng.randrange(12, 90))
@@ -297,13 +282,19 @@ def test_random_z_star_chains(seed, mode):
 
     a, b = u1, u2
     box = tuple(slice(l, h) for l, h in zip(lo, hi))
-    for _ in range(2 * rng.randrange(2, 7)):  # >= 4 sweeps: chains come in pairs
+    sweeps = 2 * rng.randrange(2, 7)  # >= 4 sweeps: chains come in pairs
+    for _ in range(sweeps):
         prog.assign(b, box, tree(a))
         a, b = b, a
     want = strict_execute_dag(prog.dag, prog.shapes, prog.dtypes)
+    from paper_2512_19851_b200 import codegen, temporal
+    from paper_2512_19851_b200.analysis import compile_plan
+    sig = codegen.stmt_sig(compile_plan(prog.dag.nodes[-1], prog.dag.ast_table).statements[0], 3)
+    fits = temporal.eligible(sig, dtype)
     job, _ = run_program(prog)
     try:
-        assert _ran(job, mode)
+        assert _ran(job, mode) == (fits and _chains(mode, sweeps))
+        assert fits or mode == "k4", "every random K = 2 case must be chainable"
         for aid in prog.shapes:
             assert bits_equal(job.fetch(aid), want[aid]), (seed, aid)
     finally:

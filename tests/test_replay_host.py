@@ -64,3 +64,24 @@ def test_replay_bookkeeping_equals_fresh_execution():
         for a, b in zip(stats_a, stats_b):
             assert (a.nodes_executed, a.kernel_launches, a.rounds, a.net_messages) == \
                    (b.nodes_executed, b.kernel_launches, b.rounds, b.net_messages)
+
+
+def test_replay_cache_is_bounded_and_drops_stale_layouts(monkeypatch):
+    """the replay cache (and the CUDA graphs it owns) is capped,
+    and entries of an older buffer layout are released."""
+    from paper_2512_19851_b200.executor import GpuExecutor
+
+    closed = []
+
+    class G:
+        def close(self):
+            closed.append(self)
+
+    ex = GpuExecutor.__new__(GpuExecutor)
+    ex._replay = {}
+    monkeypatch.setattr(GpuExecutor, "REPLAY_CAP", 4)
+    for k in range(10):
+        ex._remember((bytes([k]), (1, ())), {"graph": G()})
+    assert len(ex._replay) == 4 and len(closed) == 6
+    ex._remember((b"new", (2, ())), {"graph": G()})
+    assert list(ex._replay) == [(b"new", (2, ()))] and len(closed) == 10

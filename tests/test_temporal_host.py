@@ -20,7 +20,7 @@ def _small_grids_chain(monkeypatch):
     monkeypatch.setattr(temporal, "MIN_POINTS", 0)  # chains at test sizes (default: large grids only)
 
 
-def _executor(shapes, workers=1, odf=1, temporal_on=True, resident_on=False, rsm_on=False):
+def _executor(shapes, workers=1, odf=1, temporal_on=True, rsm_on=False):
     dev = FakeDevice()
     shape = next(iter(shapes.values()))
     decomp = decompose(shape, workers, odf)
@@ -31,9 +31,7 @@ def _executor(shapes, workers=1, odf=1, temporal_on=True, resident_on=False, rsm
     mgr = GpuExchangeManager(store, 0, decomp.owner_map(workers))
     ex = GpuExecutor(store, mgr)
     ex.temporal = temporal_on
-    ex.resident = resident_on
     ex.resident_smem = rsm_on
-    ex.wave = False
     return ex, store, mgr, dev
 
 
@@ -160,109 +158,6 @@ def test_z_star_required():
 
 
 # ---------------------------------------------------------------------------
-# resident chains (resident.py): whole L2-resident runs in one launch
-
-@pytest.mark.parametrize("iters", [2, 3, 7, 100])
-def test_resident_run_is_one_launch(iters):
-    setup, step = _heat(iters)
-    ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=True)
-    ex.execute_batch(setup.dag)
-    dev.log.clear()
-    stats = ex.execute_batch(step.dag)
-    names = _names(dev)
-    assert names == ["est_resident"]
-    assert stats.kernel_launches == iters and stats.nodes_executed == iters
-
-
-def test_resident_bookkeeping_matches_node_by_node():
-    from paper_2512_19851_b200.programs import laplace_iteration_statements, laplace_program
-    setup, step = DagProgram(), DagProgram()
-    names = laplace_program(setup, 64, 0)
-    for a in sorted(setup.shapes):
-        step.builder.declare_array(a, setup.shapes[a])
-    laplace_iteration_statements(step, names["u"], names["scratch"], 9)
-    res = []
-    for on in (True, False):
-        ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=on)
-        ex.execute_batch(setup.dag)
-        st = [ex.execute_batch(step.dag, b"k") for _ in range(4)]
-        res.append(({a: (store.local_epoch(a), store.ghost_epoch(a)) for a in store.arrays},
-                    dict(mgr.rounds_started),
-                    [(s.nodes_executed, s.kernel_launches, s.rounds, s.net_messages) for s in st]))
-    assert res[0] == res[1]
-
-
-def test_resident_needs_l2_fit_and_single_tile(monkeypatch):
-    from paper_2512_19851_b200 import resident
-    setup, step = _heat(6, n=16)
-    plans = [compile_plan(n, step.dag.ast_table) for n in step.dag.nodes]
-    ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=True)
-    assert ex.temporal_schedule(step.dag, plans)[step.dag.nodes[0].node_id] == ("res", 6)
-    monkeypatch.setattr(resident, "L2_BUDGET", 1024)
-    ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=True)
-    assert ex.temporal_schedule(step.dag, plans) == {}
-    monkeypatch.undo()
-    ex, store, mgr, dev = _executor(setup.shapes, 1, 2, temporal_on=False, resident_on=True)
-    assert ex.temporal_schedule(step.dag, plans) == {}
-
-
-def test_resident_kernel_source():
-    from paper_2512_19851_b200 import resident
-    from paper_2512_19851_b200.programs import laplace_program
-    prog = DagProgram()
-    laplace_program(prog, 32, 1)
-    plan = compile_plan(prog.dag.nodes[-1], prog.dag.ast_table)
-    sig = codegen.stmt_sig(plan.statements[0], 2)
-    assert resident.eligible(sig, DTYPE_F64, 2)
-    src, name, block, smem, geo = resident.source(sig, DTYPE_F64, 2)
-    assert name == "est_resident" and "ld.acquire.gpu" in src and "__ldcg" in src and "__stcg" in src
-    assert "__dadd_rn" in src and smem <= 48 * 1024
-
-
-@pytest.mark.parametrize("iters", [2, 5, 8])
-def test_wave_pairs(iters):
-    setup, step = _heat(iters)
-    ex, store, mgr, dev = _executor(setup.shapes, temporal_on=False, resident_on=False)
-    ex.wave = True
-    ex.execute_batch(setup.dag)
-    dev.log.clear()
-    stats = ex.execute_batch(step.dag)
-    names = _names(dev)
-    assert names.count("est_wave") == iters // 2
-    assert names.count("est_stream") == iters % 2
-    assert stats.kernel_launches == iters
-
-
-def test_wave_kernel_source():
-    from paper_2512_19851_b200 import wavefront
-    prog = DagProgram()
-    heat3d_setup(prog, 32)
-    prog.assign(1, (slice(1, -1),) * 3, heat3d_tree(0))
-    plan = compile_plan(prog.dag.nodes[-1], prog.dag.ast_table)
-    sig = codegen.stmt_sig(plan.statements[0], 3)
-    assert wavefront.eligible(sig, DTYPE_F64)
-    src, name, block, smem, geo = wavefront.source(sig, DTYPE_F64)
-    assert name == "est_wave" and "fence.proxy.async.global" in src and "ld.acquire.gpu" in src
-    assert "atomicAdd(ctr, 1u)" in src and smem <= 227 * 1024
-
-
-@pytest.mark.parametrize("nxy,nzb", [(1, 1), (3, 1), (4, 2), (5, 3), (64, 16), (2, 7)])
-def test_wave_ticket_order_is_deadlock_free(nxy, nzb):
-    """Every ticket is dispensed once and each sweep-2 item's dependencies
-    (all sweep-1 tiles of z-blocks b-1..b+1) hold earlier tickets."""
-    from paper_2512_19851_b200.wavefront import decode
-    n1 = nxy * nzb
-    pos = {}
-    for t in range(2 * n1):
-        pos[decode(t, nxy, n1, 2)] = t
-    assert len(pos) == 2 * n1
-    for i in range(n1):
-        zb = i // nxy
-        for b in range(max(zb - 1, 0), min(zb + 1, nzb - 1) + 1):
-            assert all(pos[(1, b * nxy + k)] < pos[(2, i)] for k in range(nxy))
-
-
-# ---------------------------------------------------------------------------
 # resident-smem chains (resident.py): small rank-2 runs held in shared memory
 
 def _laplace(n, iters):
@@ -365,4 +260,26 @@ def test_b_written_only_by_the_last_chain_of_a_run():
     ex.execute_batch(step.dag)
     tb = [p for e, p in zip(dev.log, dev.params) if e[2] == "est_tb"]
     assert len(tb) == 4
-    assert [struct.unpack_from("<i", p, 128 + 40 + 14 * 4)[0] for p in tb] == [0, 0, 0, 1]
+    assert [struct.unpack_from("<i", p, 128 + 24 + 14 * 4)[0] for p in tb] == [0, 0, 0, 1]
+
+
+def test_self_dependent_statement_is_rejected_before_any_launch():
+    """ADVICE r1: the in-process API has no coordinator validating the DAG;
+    A[S] = f(A[S + o]) must raise SelfDependency (ir.py:354-357) instead of
+    being scheduled as a chain whose two arrays share one buffer."""
+    from paper_2512_19851_b200.errors import SelfDependency
+    from paper_2512_19851_b200.ir import Dag, DagNode, Statement, compute_edges
+
+    setup, step = _heat(4)
+    ex, store, mgr, dev = _executor(setup.shapes)
+    ex.execute_batch(setup.dag)
+    good = step.dag.nodes[0]
+    st = good.statements[0]
+    bad_st = Statement(st.ast_id, st.output, st.output_slice, tuple(st.output for _ in st.inputs))
+    nodes = [DagNode(0, [bad_st]), DagNode(1, [bad_st])]
+    dag = Dag(nodes, compute_edges(nodes), step.dag.ast_table)
+    dev.log.clear()
+    with pytest.raises(SelfDependency):
+        ex.execute_batch(dag)
+    assert not [e for e in dev.log if e[0] == "launch"]
+    assert ex._chain_candidate(compile_plan(nodes[0], dag.ast_table)) is None
