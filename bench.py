@@ -299,6 +299,35 @@ def run_reference_arm(args, w):
 # --------------------------------------------------------------------------
 # GPU arm
 
+def parity_check(w, skeleton: str = "auto") -> dict:
+    """The benchmarked path validated at the benchmarked size: a fresh job
+    runs the setup and ONE bench step (the same DAG bytes, kernels and chain
+    schedule as the timed steps) and the whole-array content hash of every
+    array (est_hash_box) is compared with the strict C oracle
+    (oracle/strict_eval.c, all host cores) run over the same DAGs — i.e.
+    bit-equality of every element. Test infrastructure: only the checker
+    reads the oracle."""
+    from oracle.oracle import content_hash, strict_execute_dag
+    from paper_2512_19851_b200.wire import decode_dag
+
+    t0 = time.perf_counter()
+    job, prog, arrays = build_job(w, 1, 0, skeleton)
+    try:
+        blob = step_dag(w, prog.shapes, prog.dtypes, arrays)
+        job.run_bytes(blob)
+        got = {a: job.hash(a) for a in sorted(prog.shapes)}
+        kinds = "tb chains" if job.executors[0]._scratch else "node kernels"
+    finally:
+        job.close()
+    want = strict_execute_dag(prog.dag, prog.shapes, prog.dtypes, threads=host_threads())
+    strict_execute_dag(decode_dag(blob), prog.shapes, prog.dtypes, arrays=want, threads=host_threads())
+    ok = all(got[a] == content_hash(want[a]) for a in got)
+    return {"ok": ok, "method": "setup + 1 bench step (%d iterations, %s) on a fresh job; whole-array "
+                                "content hash of every array vs the strict C oracle (bit-equality)"
+                                % (w["iters_per_step"], kinds),
+            "arrays": len(got), "seconds": round(time.perf_counter() - t0, 1)}
+
+
 def build_job(w, world: int, rank: int, skeleton: str = "auto"):
     from paper_2512_19851_b200.programs import DagProgram, heat3d_setup, laplace_program, wave2d_setup
     from paper_2512_19851_b200.session import GpuJob
@@ -356,6 +385,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skeleton", default="auto", choices=["auto", "point", "stream"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-check", action="store_true",
+                    help="skip the parity check of one bench step against the strict C oracle")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -551,12 +582,14 @@ def main():
         "gpu_launches": gpu_launches,
         "clocks": clock,
     }
+    job.close()
+    if world == 1 and not args.no_check:
+        line["check"] = parity_check(w, args.skeleton)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample(w)
         line["cpu_baseline"].pop("seconds", None)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    job.close()
     if dist:
         dist.destroy_process_group()
 

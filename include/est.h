@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define EST_ABI_VERSION 6
+#define EST_ABI_VERSION 7
 
 typedef struct est_ctx est_ctx;       /* one device + compute/copy streams      */
 typedef struct est_module est_module; /* an NVRTC-compiled, loaded cubin        */
@@ -68,6 +68,16 @@ int est_copy_box(est_ctx *ctx, const est_box *box, int elem_size, int stream);
  * memory). Replaces ExchangeManager.pack/_unpack + co-located strip copies
  * (exchange.py:147-165, 192-197). */
 int est_copy_boxes(est_ctx *ctx, const est_box *boxes, int n, int elem_size, int stream);
+
+/* Position-keyed content hash of one box (src side of `box`; dst unused):
+ * sum over its elements of mix64(bits + 0x9e3779b97f4a7c15 * (g + 1)) mod 2^64,
+ * g = the element's global C-order index in an array of dims `gdims`, the box
+ * starting at global `origin` (z, y, x). Partial hashes of any decomposition
+ * sum to the whole array's hash. Synchronous on the compute stream. Extension
+ * (no reference counterpart): whole-array bit-equality checks across rescales
+ * (the reference compares fetched arrays, pkg/tests/test_acceptance.py:266-315). */
+int est_hash_box(est_ctx *ctx, const est_box *box, const int64_t origin[3], const int64_t gdims[3],
+                 int elem_size, uint64_t *out);
 
 /* ---- kernels: replaces evaluate_statement (executor.py:86-176) ------------
  * src is a generated sm_100a stencil skeleton instance (paper_2512_19851_b200/

@@ -283,3 +283,36 @@ def bits_equal(a: np.ndarray, b: np.ndarray) -> bool:
         return False
     iv = np.uint64 if a.dtype == np.float64 else np.uint32
     return bool(np.array_equal(a.view(iv)[~na], b.view(iv)[~nb]))
+
+
+# --------------------------------------------------------------------------
+# position-keyed content hash (restates include/est.h est_hash_box for tests)
+
+def content_hash(arr: np.ndarray, threads: int = 0) -> int:
+    """sum_i mix64(bits_i + 0x9e3779b97f4a7c15 * (i + 1)) mod 2^64 over the
+    C-order elements of `arr` (float64 bits, or float32 bits zero-extended);
+    strict_eval.c oracle_content_hash (OpenMP)."""
+    a = np.ascontiguousarray(arr)
+    lib = _lib()
+    lib.oracle_content_hash.restype = ctypes.c_uint64
+    return int(lib.oracle_content_hash(ctypes.c_void_p(a.ctypes.data), ctypes.c_int64(a.size),
+                                       ctypes.c_int(a.dtype.itemsize), ctypes.c_int(threads)))
+
+
+def content_hash_numpy(arr: np.ndarray, chunk: int = 1 << 24) -> int:
+    """The same hash in numpy (pins the C route in tests/test_oracle_pinned.py)."""
+    a = np.ascontiguousarray(arr)
+    flat = (a.view(np.uint64) if a.dtype == np.float64 else a.view(np.uint32)).ravel()
+    total = 0
+    with np.errstate(over="ignore"):
+        for lo in range(0, flat.size, chunk):
+            bits = flat[lo:lo + chunk].astype(np.uint64)
+            x = bits + np.uint64(0x9E3779B97F4A7C15) * (np.arange(lo, lo + bits.size, dtype=np.uint64)
+                                                        + np.uint64(1))
+            x ^= x >> np.uint64(30)
+            x *= np.uint64(0xBF58476D1CE4E5B9)
+            x ^= x >> np.uint64(27)
+            x *= np.uint64(0x94D049BB133111EB)
+            x ^= x >> np.uint64(31)
+            total = (total + int(np.sum(x, dtype=np.uint64))) % (1 << 64)
+    return total

@@ -107,3 +107,25 @@ int oracle_max_threads(void) {
     return 1;
 #endif
 }
+
+/* Position-keyed content hash (restates include/est.h est_hash_box for the
+ * checker): sum over i of mix64(bits_i + 0x9e3779b97f4a7c15 * (i + 1)) mod 2^64,
+ * bits = the float64 bit pattern (elem 8) or the zero-extended float32 one. */
+static inline uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+
+uint64_t oracle_content_hash(const void *data, int64_t n, int elem, int threads) {
+    uint64_t total = 0;
+    _Pragma("omp parallel for reduction(+:total) schedule(static) num_threads(threads > 0 ? threads : omp_get_max_threads())")
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t bits = elem == 8 ? ((const uint64_t *)data)[i] : (uint64_t)((const uint32_t *)data)[i];
+        total += mix64(bits + 0x9e3779b97f4a7c15ULL * (uint64_t)(i + 1));
+    }
+    return total;
+}

@@ -14,7 +14,7 @@ from .errors import from_code
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libest.so")
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 u64, i64, i32, u32 = C.c_uint64, C.c_int64, C.c_int, C.c_uint32
 vp = C.c_void_p
@@ -43,6 +43,7 @@ _SIGS = {
     "est_host_free": (i32, [u64]),
     "est_copy_box": (i32, [vp, P(EstBox), i32, i32]),
     "est_copy_boxes": (i32, [vp, P(EstBox), i32, i32, i32]),
+    "est_hash_box": (i32, [vp, P(EstBox), P(i64), P(i64), i32, P(u64)]),
     "est_module_compile": (i32, [vp, C.c_char_p, P(C.c_char_p), i32, C.c_char_p, P(vp), P(i32)]),
     "est_module_precompile": (i32, [C.c_char_p, P(C.c_char_p), i32, C.c_char_p, P(i32)]),
     "est_module_load_cubin": (i32, [vp, vp, P(vp)]),

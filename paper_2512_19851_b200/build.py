@@ -105,6 +105,12 @@ def install_reference(src: str = "/root/reference/pkg") -> str | None:
     import tempfile
 
     dst = os.path.join(ROOT, "baseline", "_ref")
+    tests = os.path.join(dst, "ref_tests")
+    if os.path.isdir(os.path.join(src, "tests")) and not os.path.isdir(tests) and os.path.isdir(dst):
+        # the reference's own runtime / daemon / acceptance suites, run against
+        # the GPU workers by tests/test_gpu_reference_suites.py (git-ignored like
+        # the install itself; travels to the GPU box with baseline/_ref)
+        shutil.copytree(os.path.join(src, "tests"), tests)
     if os.path.isdir(os.path.join(dst, "elastencil")) or not os.path.isdir(src):
         return dst if os.path.isdir(dst) else None
     tmp = tempfile.mkdtemp(prefix="refpkg-")
@@ -113,6 +119,7 @@ def install_reference(src: str = "/root/reference/pkg") -> str | None:
         subprocess.run([sys.executable, "-m", "pip", "install", "--no-index", "--no-build-isolation",
                         "--no-deps", "--target", dst, os.path.join(tmp, "pkg")],
                        check=True, capture_output=True)
+        shutil.copytree(os.path.join(src, "tests"), tests)
         return dst
     except (OSError, subprocess.CalledProcessError) as exc:
         print(f"[build] reference install skipped: {exc}", file=sys.stderr)

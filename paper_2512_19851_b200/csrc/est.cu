@@ -257,7 +257,11 @@ extern "C" int est_copy_box(est_ctx *c, const est_box *b, int elem, int s) {
     return 0;
 }
 
-// Batched small-box copy: one CTA row per box, grid-stride over elements.
+// Batched small-box copy: one grid row (blockIdx.y) per box. Boxes whose rows
+// are at least a warp wide copy one row per warp (the row's plane / row index
+// computed once per row, 16-byte vectors when source and destination share
+// their alignment: the contiguous z-faces of rank-3 slabs, y-strips); narrow
+// boxes (x-strips of depth d) copy element-wise.
 #define EST_MAX_BOXES 48
 struct BoxBatch {
     int n;
@@ -265,11 +269,38 @@ struct BoxBatch {
 };
 
 template <typename W>
+__device__ __forceinline__ void copy_row(const W *__restrict__ s, W *__restrict__ d, int64_t nx, int lane) {
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(s), da = reinterpret_cast<uintptr_t>(d);
+    if (((sa ^ da) & 15) == 0 && nx * (int64_t)sizeof(W) >= 64) {
+        const int64_t head = (int64_t)(((16 - (sa & 15)) & 15) / sizeof(W));
+        const int64_t nvec = (nx - head) * (int64_t)sizeof(W) / 16;
+        const int64_t tail0 = head + nvec * (16 / (int64_t)sizeof(W));
+        if (lane < head) d[lane] = s[lane];
+        const uint4 *sv = reinterpret_cast<const uint4 *>(s + head);
+        uint4 *dv = reinterpret_cast<uint4 *>(d + head);
+        for (int64_t i = lane; i < nvec; i += 32) dv[i] = sv[i];
+        for (int64_t x = tail0 + lane; x < nx; x += 32) d[x] = s[x];
+    } else {
+        for (int64_t x = lane; x < nx; x += 32) d[x] = s[x];
+    }
+}
+
+template <typename W>
 __global__ void __launch_bounds__(256) copy_boxes_kernel(const __grid_constant__ BoxBatch bb) {
     const est_box &b = bb.box[blockIdx.y];
-    const int64_t nrow = b.nx, rows = b.ny * b.nz, total = nrow * rows;
     const W *__restrict__ src = reinterpret_cast<const W *>(b.src);
     W *__restrict__ dst = reinterpret_cast<W *>(b.dst);
+    const int64_t rows = b.ny * b.nz;
+    if (b.nx >= 32) {
+        const int lane = threadIdx.x & 31;
+        const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+        for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+            const int64_t z = r / b.ny, y = r - z * b.ny;
+            copy_row<W>(src + z * b.src_pz + y * b.src_py, dst + z * b.dst_pz + y * b.dst_py, b.nx, lane);
+        }
+        return;
+    }
+    const int64_t nrow = b.nx, total = nrow * rows;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = i / nrow, x = i - r * nrow;
@@ -303,6 +334,66 @@ extern "C" int est_copy_boxes(est_ctx *c, const est_box *boxes, int n, int elem,
             copy_boxes_kernel<unsigned int><<<grid, 256, 0, pick(c, s)>>>(bb);
         CUDA_TRY(cudaGetLastError());
     }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Position-keyed content hash of a box (a tile interior): sum over elements of
+// mix(bits + K * (global linear index + 1)) mod 2^64, so partial hashes of any
+// decomposition add up to the same value (tests/test_gpu_hash.py restates it
+// in numpy). Used to compare whole arrays across rescales without a D2H copy.
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+
+template <typename W>
+__global__ void __launch_bounds__(256) hash_box_kernel(est_box b, int64_t oz, int64_t oy, int64_t ox,
+                                                       int64_t gy, int64_t gx, unsigned long long *out) {
+    const W *__restrict__ src = reinterpret_cast<const W *>(b.src);
+    const int64_t rows = b.ny * b.nz;
+    const int lane = threadIdx.x & 31;
+    uint64_t acc = 0;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+        const int64_t z = r / b.ny, y = r - z * b.ny;
+        const W *row = src + z * b.src_pz + y * b.src_py;
+        const int64_t g0 = ((oz + z) * gy + (oy + y)) * gx + ox;
+        for (int64_t x = lane; x < b.nx; x += 32)
+            acc += mix64((uint64_t)row[x] + 0x9e3779b97f4a7c15ULL * (uint64_t)(g0 + x + 1));
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) atomicAdd(out, (unsigned long long)acc);
+}
+
+extern "C" int est_hash_box(est_ctx *c, const est_box *b, const int64_t origin[3], const int64_t gdims[3],
+                            int elem, uint64_t *out) {
+    *out = 0;
+    if (elem != 4 && elem != 8) return fail(14, "elem size %d unsupported", elem);
+    if (b->nx * b->ny * b->nz <= 0) return 0;
+    CUDA_TRY(cudaSetDevice(c->device));
+    unsigned long long *d = nullptr;
+    CUDA_TRY(cudaMallocAsync(&d, sizeof(*d), pick(c, 0)));
+    CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(*d), pick(c, 0)));
+    int64_t rows = b->ny * b->nz, blocks = (rows + 7) / 8;
+    if (blocks > 8 * 148) blocks = 8 * 148;
+    if (elem == 8)
+        hash_box_kernel<unsigned long long><<<(unsigned)blocks, 256, 0, pick(c, 0)>>>(
+            *b, origin[0], origin[1], origin[2], gdims[1], gdims[2], d);
+    else
+        hash_box_kernel<unsigned int><<<(unsigned)blocks, 256, 0, pick(c, 0)>>>(
+            *b, origin[0], origin[1], origin[2], gdims[1], gdims[2], d);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, pick(c, 0)));
+    CUDA_TRY(cudaFreeAsync(d, pick(c, 0)));
+    CUDA_TRY(cudaStreamSynchronize(pick(c, 0)));
+    *out = h;
     return 0;
 }
 

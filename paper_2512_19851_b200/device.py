@@ -151,6 +151,14 @@ class Device:
         check(self.lib.est_copy_boxes(self.ctx, arr, len(boxes), elem, stream))
         self.launches += (len(boxes) + 47) // 48
 
+    def hash_box(self, box, origin, gdims, elem: int) -> int:
+        """Position-keyed content hash of `box`'s source side (est_hash_box)."""
+        out = C.c_uint64(0)
+        check(self.lib.est_hash_box(self.ctx, C.byref(box), (C.c_int64 * 3)(*origin),
+                                    (C.c_int64 * 3)(*gdims), elem, C.byref(out)))
+        self.launches += 1
+        return out.value
+
     # -- sync / events ------------------------------------------------------
     def sync(self) -> None:
         check(self.lib.est_ctx_sync(self.ctx))

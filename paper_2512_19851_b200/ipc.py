@@ -380,6 +380,15 @@ class IpcGpuJob:
                 out[tuple(slice(a - lo, b - lo) for (a, b), (lo, _) in zip(piece, bounds))] = block
         return out
 
+    def hash_local(self, array: int) -> int:
+        """This rank's partial of the whole-array content hash (its tiles)."""
+        self.dev.sync()
+        return self.store.hash(array) if self.store is not None and self.store.tiles else 0
+
+    def hash(self, array: int) -> int:
+        """Collective: the whole array's position-keyed content hash."""
+        return sum(self._all_gather(self.hash_local(array))) % (1 << 64)
+
     def rounds_by_array(self) -> dict:
         mine = self.manager.snapshot_stats()["rounds"] if self.store.tiles else None
         allr = [r for r in self._all_gather(mine) if r is not None]

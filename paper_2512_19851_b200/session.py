@@ -131,6 +131,12 @@ class GpuJob:
                 out[tuple(slice(a - lo, b - lo) for (a, b), (lo, _) in zip(piece, bounds))] = block
         return out
 
+    def hash(self, array: int) -> int:
+        """Whole-array position-keyed content hash (est_hash_box), summed over
+        every worker's tiles: a decomposition-independent fingerprint."""
+        self.sync()
+        return sum(st.hash(array) for st in self.stores if st.tiles) % (1 << 64)
+
     def rounds_by_array(self) -> dict:
         counts = [m.snapshot_stats()["rounds"] for m in self.managers if m.store.tiles]
         for c in counts[1:]:

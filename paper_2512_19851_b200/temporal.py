@@ -63,6 +63,9 @@ MAX_RADIUS = 2
 SMEM_BUDGET = 220 * 1024
 SMEM_PER_SM = 228 * 1024
 SKIP_MID_B = os.environ.get("EST_TB_SKIPB", "1") == "1"
+# measurement probes (wrong results, never scheduled by default): "noshared"
+# replaces every in-plane operand by the centre value (no shared-memory loads)
+PROBE = os.environ.get("EST_TB_PROBE", "")
 
 
 @dataclass(frozen=True)
@@ -75,6 +78,7 @@ class TbCfg:
     zchunk: int = 192       # target planes per item (chunks are balanced)
     l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
     persistent: bool = True  # one CTA per SM slot looping over items
+    hoist: bool = False     # issue every step's shared-memory loads at the top of a plane iteration
 
 
 def _env_cfg() -> TbCfg:
@@ -83,7 +87,7 @@ def _env_cfg() -> TbCfg:
     return TbCfg(k=int(e("EST_TB_K", d.k)), bx=int(e("EST_TB_BX", d.bx)), by=int(e("EST_TB_BY", d.by)),
                  rpt=int(e("EST_TB_RPT", d.rpt)), prefetch=int(e("EST_TB_PREFETCH", d.prefetch)),
                  zchunk=int(e("EST_TB_ZCHUNK", d.zchunk)), l2promo=int(e("EST_TB_L2PROMO", d.l2promo)),
-                 persistent=e("EST_TB_PERSISTENT", "1") == "1")
+                 persistent=e("EST_TB_PERSISTENT", "1") == "1", hoist=e("EST_TB_HOIST", "0") == "1")
 
 
 DEFAULT = _env_cfg()
@@ -194,6 +198,8 @@ class _Emitter:
             for v in range(V):
                 def load(slot, off3, r=r, v=v):
                     dz, dy, dx = off3
+                    if PROBE == "noshared":  # measurement probe: in-plane operands from registers
+                        dy, dx = 0, 0
                     if dz != 0 or (dy == 0 and dx == 0):
                         return f"c{j - 1}_{r}_{v}_{(rz + dz + mm) % Z}"
                     rr, xc = r + dy, v + dx
@@ -201,24 +207,42 @@ class _Emitter:
                         return f"c{j - 1}_{rr}_{xc}_{(rz + mm) % Z}"
                     g, comp = xc // V, xc % V
                     need.setdefault((rr, g), set()).add(comp)
-                    return f"n_{self._rn(rr)}_{self._rn(g)}_{comp}"
+                    return f"n{j}_{self._rn(rr)}_{self._rn(g)}_{comp}"
                 lines, res = _emit_expr(self.st, self.dtype, load)
                 body.append((r, v, lines, res))
         return body, need
 
-    def emit_smem_loads(self, ind: str, need: dict, base: str, pitch: int) -> None:
-        """One vector load per group with >= 2 needed components, else scalars."""
+    def emit_smem_loads(self, ind: str, j: int, need: dict, base: str, pitch: int) -> None:
+        """Step j's shared-memory operands: one vector load per group with >= 2
+        needed components, else scalars.
+
+        A row's west / east neighbours (the last component of the vector to
+        the left, the first of the vector to the right) are loaded as a
+        crossed pair: half of the lanes of every bank phase (8 lanes for
+        64-bit loads, which the LSU serves per half-warp; 16 for 32-bit)
+        fetch west then east, the other half east then west. At a 16-byte
+        lane stride each scalar load of one neighbour alone uses half of the
+        banks twice; the crossed halves use disjoint bank sets."""
         V = self.lay["V"]
+        need = dict(need)
+        for rr in sorted({k[0] for k in need}):
+            if need.get((rr, -1)) == {V - 1} and need.get((rr, 1)) == {0}:
+                del need[(rr, -1)], need[(rr, 1)]
+                t = f"{j}_{self._rn(rr)}"
+                self.a(f"{ind}const {self.T} xa{t} = {base}[{rr * pitch - 1} + sw];")
+                self.a(f"{ind}const {self.T} xb{t} = {base}[{rr * pitch + V} - sw];")
+                self.a(f"{ind}const {self.T} n{t}_m1_{V - 1} = xw ? xb{t} : xa{t};")
+                self.a(f"{ind}const {self.T} n{t}_1_0 = xw ? xa{t} : xb{t};")
         for (rr, g), comps in sorted(need.items()):
             off = rr * pitch + g * V
-            tag = f"{self._rn(rr)}_{self._rn(g)}"
+            tag = f"{j}_{self._rn(rr)}_{self._rn(g)}"
             if len(comps) >= 2:
-                self.a(f"{ind}const {self.VT} q_{tag} = *reinterpret_cast<const {self.VT}*>({base} + ({off}));")
+                self.a(f"{ind}const {self.VT} q{tag} = *reinterpret_cast<const {self.VT}*>({base} + ({off}));")
                 for c in sorted(comps):
-                    self.a(f"{ind}const {self.T} n_{tag}_{c} = q_{tag}.{'xyzw'[c]};")
+                    self.a(f"{ind}const {self.T} n{tag}_{c} = q{tag}.{'xyzw'[c]};")
             else:
                 (c,) = tuple(comps)
-                self.a(f"{ind}const {self.T} n_{tag}_{c} = {base}[{off + c}];")
+                self.a(f"{ind}const {self.T} n{tag}_{c} = {base}[{off + c}];")
 
     # -- kernel ---------------------------------------------------------------
     def source(self) -> str:
@@ -231,7 +255,7 @@ class _Emitter:
         NT, s0, E = lay["nt"], lay["s0"], lay["elem"]
         a = self.a
         NW = NT // 32
-        minb = max(1, min(blocks_per_sm(lay["smem"], NT), 65536 // ((NT + 32) * 80)))
+        minb = max(1, min(blocks_per_sm(lay["smem"], NT), 65536 // ((NT + 32) * 96)))
         lay["min_blocks"] = minb
         a(f'// generated by paper_2512_19851_b200/temporal.py — skeleton "tb" (K={K} fused sweeps, '
           f'V={V} vectors) {cfg} py={self.py} pz={self.pz} xoff={self.xoff}')
@@ -294,6 +318,9 @@ class _Emitter:
         a("  T* __restrict__ bmem = reinterpret_cast<T*>(p.bhome);")
         a("  T* __restrict__ adst = reinterpret_cast<T*>(p.adst);")
         a(f"  const bool act = tid < {lay['nact']};")
+        a(f"  const bool xw = (lane & {8 if V == 2 else 16}) != 0;  // crossed west/east neighbour loads")
+        a(f"  const int sw = xw ? {V + 1} : 0;")
+        a("  const int wb = p.wb, sz0 = p.sz0, sz1 = p.sz1, npz = p.npz;")
         a(f"  const int cc = tid % {P1}, gg = tid / {P1};  // vector column / row group in the step-1 frame")
         a(f"  const int off0 = ({e[0] - e[1]} + gg * {RPT}) * {W0} + {m[0] - m[1]} + cc * {V};  // input frame")
         a(f"  const int off1 = gg * {RPT} * {W1} + cc * {V};  // step-1 frame (rings)")
@@ -356,7 +383,7 @@ class _Emitter:
             a(f"{i3}const int t = t0 + {mm};")
             for j in range(1, K):
                 a(f"{i3}const int u{j} = zs - {(K + j) * rz} + t;  // step-{j} plane")
-                a(f"{i3}const bool zs{j} = u{j} >= p.sz0 && u{j} < p.sz1, zp{j} = u{j} >= 0 && u{j} < p.npz;")
+                a(f"{i3}const bool zs{j} = u{j} >= sz0 && u{j} < sz1, zp{j} = u{j} >= 0 && u{j} < npz;")
                 if edge:
                     # stored values outside S, prefetched before the plane's wait
                     home = "bmem" if j % 2 == 1 else "asrc"
@@ -373,20 +400,34 @@ class _Emitter:
                 a(f"{i3}    " + " ".join(f"c0_{r}_{v}_{(2 * rz + mm) % Z} = q.{'xyzw'[v]};" for v in range(V)) + " }")
             a(f"{i3}}}")
             a(f"{i3}int ir = is - {rz}; if (ir < 0) ir += {s0};  // slot of plane t - rz")
+            # with cfg.hoist every step's in-plane operands are loaded first: step 1
+            # reads the TMA plane of t - rz, step j > 1 the ring plane step j-1
+            # wrote rz iterations ago (behind the previous iteration's barrier),
+            # so all loads of the iteration are in flight before the first
+            # expression needs them (more live registers)
+            bodies, loads = {}, {}
             for j in range(1, K + 1):
-                final = j == K
-                a(f"{i3}if (t >= {2 * j * rz}) {{  // step {j}")
-                i4 = i3 + "  "
                 if j == 1:
-                    a(f"{i4}const T* P = ring0 + ir * {pl0} + off0;")
+                    ptr = f"const T* P1 = ring0 + ir * {pl0} + off0;"
                     pitch = W0
                 else:
                     R = lay["R"]
                     c = (rz + 2 * (j - 1) * rz) % R
-                    a(f"{i4}int rs = tr - {c}; if (rs < 0) rs += {R};  // ring {j - 1} slot of plane u{j}")
-                    a(f"{i4}const T* P = reinterpret_cast<const T*>(smem + {lay['rings'][j - 2]}) + "
-                      f"rs * {pl1} + off1;")
+                    ptr = (f"int rs{j} = tr - {c}; if (rs{j} < 0) rs{j} += {R};  // ring {j - 1} slot of plane u{j}\n"
+                           f"const T* P{j} = reinterpret_cast<const T*>(smem + {lay['rings'][j - 2]}) + "
+                           f"rs{j} * {pl1} + off1;")
                     pitch = W1
+                body, need = self.step_body(j, mm)
+                bodies[j] = body
+                loads[j] = (ptr, need, pitch)
+                if cfg.hoist:
+                    for ln in ptr.split("\n"):
+                        a(f"{i3}{ln}")
+                    self.emit_smem_loads(i3, j, need, f"P{j}", pitch)
+            for j in range(1, K + 1):
+                final = j == K
+                a(f"{i3}if (t >= {2 * j * rz}) {{  // step {j}")
+                i4 = i3 + "  "
                 if not final:
                     R = lay["R"]
                     c = (2 * j * rz) % R
@@ -396,8 +437,12 @@ class _Emitter:
                 else:
                     a(f"{i4}{{")
                 i5 = i4 + "  "
-                body, need = self.step_body(j, mm)
-                self.emit_smem_loads(i5, need, "P", pitch)
+                if not cfg.hoist:
+                    ptr, need, pitch = loads[j]
+                    for ln in ptr.split("\n"):
+                        a(f"{i5}{ln}")
+                    self.emit_smem_loads(i5, j, need, f"P{j}", pitch)
+                body = bodies[j]
                 for r, v, lines, res in body:
                     a(f"{i5}T o{r}_{v};")
                     a(f"{i5}{{ " + " ".join(lines) + f" o{r}_{v} = {res}; }}")
@@ -414,7 +459,7 @@ class _Emitter:
                     if final:
                         targets.append(("ap", f"in{K}_{r}"))
                     if j == K - 1:
-                        targets.append(("bp", f"p.wb && in{K}_{r} && u{j} >= zs && u{j} < zs + nzl"))
+                        targets.append(("bp", f"wb && in{K}_{r} && u{j} >= zs && u{j} < zs + nzl"))
                     for ptr, cond in targets:
                         if not edge:
                             a(f"{i5}if ({cond}) *reinterpret_cast<{VT}*>({ptr} + {r * PY}) = {vec};")
@@ -433,7 +478,8 @@ class _Emitter:
                     for r in range(RPT):
                         vals = []
                         for v in range(V):
-                            a(f"{i4}  const T s{r}_{v} = (zp{j} && in{j}_{r}) ? "
+                            guard = f"zp{j} && in{j}_{r}" + (f" && yp{r} && xp{v}" if edge else "")
+                            a(f"{i4}  const T s{r}_{v} = ({guard}) ? "
                               f"{home}[(long long)u{j} * {PZ} + gb + {r * PY + v}] : (T)0;")
                             vals.append(f"s{r}_{v}")
                         a(f"{i4}  *reinterpret_cast<{VT}*>(Wr + {r * W1}) = make_{VT}({', '.join(vals)});")

@@ -371,6 +371,22 @@ class GpuTileStore:
         header = blob_header(array, tuple(coords), ext, tile.depths[array], tile.local_epoch[array])
         return header + np.ascontiguousarray(block).astype(block.dtype.newbyteorder("<"), copy=False).tobytes()
 
+    def hash(self, array: int) -> int:
+        """Sum mod 2^64 of the position-keyed hashes of every owned tile's
+        interior (est_hash_box): equal for equal arrays under ANY
+        decomposition, so the partial sums of all workers add up to the
+        whole array's hash."""
+        info = self.arrays[array]
+        g3 = pad3(info.shape, 1)
+        total = 0
+        for coords in sorted(self.tiles):
+            buf = self.tiles[coords].buffers[array]
+            ext = self.decomp.tile_extents(info.shape)
+            box = buf.box_to(0, 0, 0, (0,) * info.rank, ext)
+            org = pad3(self.decomp.tile_origin(info.shape, coords), 0)
+            total = (total + self.dev.hash_box(box, org, g3, buf.elem)) % (1 << 64)
+        return total
+
     def adopt_blob(self, blob: bytes) -> tuple:
         """adopt_blob (grid.py:264-277): install a checkpointed tile payload.
 

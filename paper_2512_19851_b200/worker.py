@@ -4,7 +4,9 @@ Speaks the reference's internal control protocol unchanged (REGISTER 200,
 INIT 201, W_CREATE 202, W_BATCH 203, W_FETCH 204, W_MIGRATE 206,
 W_CHECKPOINT 207, W_RESTORE 208, W_EXIT 209; one REPLY_OK / REPLY_ERR per
 request, worker.py:252-294), so the unchanged reference Coordinator
-(coordinator.py) drives it. Differences behind the seam:
+(coordinator.py) drives it. One additive kind, W_HASH 210 (this worker's
+partial of a whole-array content hash, est_hash_box), lets a driver compare
+16 GiB arrays across rescales without fetching them. Differences behind the seam:
 
 * tiles live in HBM of GPU `gpu_for_slot(id)` and batches run as generated
   sm_100a kernels (executor.GpuExecutor); W_BATCH is answered as soon as the
@@ -34,7 +36,7 @@ from .errors import StencilError
 from .tiles import Decomposition
 from .wire import (
     INIT, PEER_HELLO, REGISTER, REPLY_ERR, REPLY_OK, W_BATCH, W_CHECKPOINT, W_CREATE, W_EXIT,
-    W_FETCH, W_MIGRATE, W_RESTORE, parse_json, recv_frame, send_json)
+    W_FETCH, W_HASH, W_MIGRATE, W_RESTORE, parse_json, recv_frame, send_json)
 
 log = logging.getLogger("elastencil.gpu_worker")
 
@@ -165,6 +167,9 @@ class GpuWorker:
             self._handle_checkpoint(meta)
         elif kind == W_RESTORE:
             self._handle_restore(meta)
+        elif kind == W_HASH:
+            h = self.job.hash_local(meta["array"]) if self.job is not None else 0
+            send_json(self.coord, REPLY_OK, {"hash": str(h)})
         elif kind == W_EXIT:
             self._running = False
         else:
