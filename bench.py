@@ -21,9 +21,15 @@ per-step event pairs.
            share of kernel time from a 2-step event-pair pass / its launches),
            against MEASURED_PEAKS.json hbm_gbs.
 `cpu_baseline`: the strict-order C oracle (oracle/strict_eval.c) on all host
-           cores over a bounded z-slab sample of the same grid (rank 0, N=1).
---impl reference: the reference's CPU path restated (the oracle port) timed on
-           the host cores over that bounded sample per step (rank 0 only).
+           cores over a bounded z-slab sample of the same grid (rank 0, N=1),
+           with the reference's own numpy evaluator (baseline/_ref
+           executor.evaluate_statement) on one core beside it
+           (`reference_1core`) and the host CPU model.
+--impl reference: the reference's own CPU path on the host cores, rank 0
+           only: C1 through the reference runtime (Launcher + BatchingSession,
+           worker processes); C2/C4 through the reference's evaluate_statement
+           in min(8, cores) processes on z-slabs (the runtime itself rejects
+           rank 3); C3 (fp32, which the reference lacks) the oracle port.
 """
 
 from __future__ import annotations
@@ -223,6 +229,119 @@ def cpu_sample(w, iters: int = 2, planes: int = 34, threads: int = 0) -> dict:
             "seconds": dt_s}
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_evaluator_sample(w, planes: int = 34, iters: int = 1) -> dict | None:
+    """The reference's OWN hot-path function on one core: baseline/_ref
+    `elastencil.executor.evaluate_statement` (executor.py:86-176, numpy
+    ufuncs + its ScratchPool) over a z-slab (3-D) / row-slab (2-D) of the
+    workload, the statement decoded by the reference's own wire codec and
+    compiled by its own `analysis.compile_plan`. The reference runtime rejects
+    rank-3 arrays at its client / coordinator (SURVEY.md §8d "CPU side"), so a
+    one-tile store adapter stands in for its 2-D TileStore. None when the
+    reference is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "elastencil")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from types import SimpleNamespace
+
+    import elastencil.ir as ref_ir
+    from elastencil.analysis import compile_plan as ref_compile_plan  # the reference, unmodified
+    from elastencil.executor import ScratchPool, evaluate_statement
+    from elastencil.programs import DagProgram as RefDagProgram
+
+    import paper_2512_19851_b200.programs as P
+
+    n = w["n"]
+    # the workload's statement built by the REFERENCE's DagBuilder / expression
+    # constructors (this package's program builders are sink-agnostic; their
+    # ref/cst/add/mul are swapped for the reference's while building)
+    saved = {k: getattr(P, k) for k in ("ref", "cst", "add", "mul", "sub")}
+    prog = RefDagProgram()
+    try:
+        for k in saved:
+            setattr(P, k, getattr(ref_ir, k))
+        if w["kind"] == "heat3d":
+            shape = (planes, n, n)
+            P.heat3d_program(prog, n, 1, shape=shape)
+            sample = f"{iters} Jacobi iteration(s) over a {planes}x{n}x{n} z-slab of the {n}^3 grid"
+        elif w["kind"] == "wave2d":
+            shape = (max(planes * 16, 64), n)
+            u = [prog.create_array(shape) for _ in range(3)]  # the reference evaluates in float64 only
+            prog.assign(u[2], (slice(2, -2), slice(2, -2)), P.wave2d_tree(u[0], u[1]))
+            sample = (f"{iters} wave step(s) over a {shape[0]}x{n} row-slab of the {n}^2 grid "
+                      "(float64: the reference has no fp32 path)")
+        else:
+            shape = (n, n)
+            P.laplace_program(prog, n, 1)
+            sample = f"{iters} Jacobi iteration(s) over the full {n}^2 grid"
+    finally:
+        for k, v in saved.items():
+            setattr(P, k, v)
+    dag = prog.dag
+    plan = ref_compile_plan(dag.nodes[-1], dag.ast_table).statements[0]
+    depth = tuple(2 if w["kind"] == "wave2d" else 1 for _ in shape)
+    rng = np.random.default_rng(0)
+    bufs = {a: rng.random(tuple(e + 2 * d for e, d in zip(shape, depth))) for a in prog.shapes}
+    arrays = {a: SimpleNamespace(shape=shape) for a in prog.shapes}
+    zero = (0,) * len(shape)
+    decomp = SimpleNamespace(tile_origin=lambda s, c: zero, tile_extents=lambda s: tuple(s))
+
+    def interior_view(tile, a):  # grid.py:186-190
+        return tile.buffers[a][tuple(slice(d, e - d) for d, e in zip(tile.depths[a], tile.buffers[a].shape))]
+
+    store = SimpleNamespace(arrays=arrays, decomp=decomp, interior_view=interior_view)
+    tile = SimpleNamespace(coords=zero, buffers=bufs, depths={a: depth for a in prog.shapes})
+    pool = ScratchPool()
+    evaluate_statement(plan, store, tile, pool)  # warm: scratch blocks, page faults
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        evaluate_statement(plan, store, tile, pool)
+    dt_s = time.perf_counter() - t0
+    lups = int(np.prod([b - a for a, b in plan.output_slice_bounds])) * iters
+    return {"value": lups / dt_s / 1e9, "unit": "GLUP/s", "cores": 1, "kind": "reference",
+            "sample": sample + " through baseline/_ref elastencil.executor.evaluate_statement",
+            "seconds": dt_s}
+
+
+def _ref_eval_proc(w, planes, iters, barrier, q):
+    barrier.wait()
+    q.put(reference_evaluator_sample(w, planes, iters))
+
+
+def reference_evaluator_parallel(w, procs: int, planes: int = 8, iters: int = 1) -> dict | None:
+    """`reference_evaluator_sample` in `procs` concurrent processes, each on
+    its own slab - the way the reference runtime spreads tiles over one worker
+    process per core (worker.py:428-431; its bench caps workers at 8).
+    Aggregate GLUP/s = all processes' points / the slowest one's time."""
+    import multiprocessing as mp
+
+    if reference_evaluator_sample is None or not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "elastencil")):
+        return None
+    ctx = mp.get_context("fork")
+    bar, q = ctx.Barrier(procs), ctx.Queue()
+    ps = [ctx.Process(target=_ref_eval_proc, args=(w, planes, iters, bar, q)) for _ in range(procs)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join()
+    slow = max(r["seconds"] for r in res)
+    total = sum(r["value"] * r["seconds"] for r in res)  # GLUP
+    return {"value": total / slow, "unit": "GLUP/s", "cores": procs, "kind": "reference",
+            "sample": f"{procs} processes, each: " + res[0]["sample"], "seconds": slow}
+
+
 def reference_runtime_sample(w, workers: int) -> dict | None:
     """C1 through the reference's OWN runtime and public API (BASELINE.md §3:
     Launcher + BatchingSession, flush 100, as pkg/src/elastencil/bench.py
@@ -272,6 +391,29 @@ def run_reference_arm(args, w):
             }
             print(json.dumps(line), flush=True)
             return
+    procs = min(8, host_threads())
+    if w["kind"] != "wave2d" and reference_evaluator_parallel(w, procs, planes=34, iters=1) is not None:
+        # rank 3 (and the 2-D fallback): the reference's own evaluate_statement
+        vals = []
+        t0 = time.perf_counter()
+        last = None
+        for _ in range(args.steps):
+            last = reference_evaluator_parallel(w, procs, planes=34, iters=2)
+            vals.append(last["value"])
+        wall = time.perf_counter() - t0
+        value = statistics.median(vals)
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "GLUP/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": 1,
+            "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic",
+            "config": {"workload": w["label"], "grid": [w["n"]] * (3 if w["kind"] == "heat3d" else 2)},
+            "cpu_baseline": {"value": value, "unit": "GLUP/s", "cores": procs, "kind": "reference",
+                             "sample": "each step: " + last["sample"], "cpu_model": cpu_model()},
+            "e2e": {"value": value, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
     planes = 34 if w["kind"] == "heat3d" else 8
     for _ in range(args.warmup):
         cpu_sample(w, iters=1, planes=planes)
@@ -588,6 +730,11 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample(w)
         line["cpu_baseline"].pop("seconds", None)
+        line["cpu_baseline"]["cpu_model"] = cpu_model()
+        ref1 = reference_evaluator_sample(w, planes=34 if w["kind"] == "heat3d" else 8, iters=3)
+        if ref1 is not None:  # the reference's own numpy evaluator, one core (SURVEY.md §8d CPU side)
+            ref1.pop("seconds", None)
+            line["cpu_baseline"]["reference_1core"] = ref1
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
