@@ -14,8 +14,11 @@ workload whose arrays fit L2 (c1) gets a 512 MB write between steps, outside
 per-step event pairs.
 
 `value`  : device time (CUDA events on the compute stream), max over ranks.
-`e2e`    : host wall clock through the public API per step (DAG bytes in,
-           one result plane fetched to host), max over ranks.
+`e2e`    : host wall clock per step through the reference-facing seam (N=1:
+           the reference Coordinator + a GPU worker process, W_BATCH frame in,
+           W_FETCH of one result plane out; `e2e.in_process` = the same through
+           the in-process API GpuJob.run_bytes; N>1: the in-process API on
+           every rank), max over ranks.
 `roofline`: the dominant kernel kind, achieved = algorithmic bytes per launch /
            its average launch duration in the timed region (device time x its
            share of kernel time from a 2-step event-pair pass / its launches),
@@ -518,6 +521,55 @@ def step_dag(w, prog_shapes, dtypes, arrays):
     return encode_dag(prog.dag)
 
 
+def seam_e2e(w, steps: int, warmup: int) -> dict | None:
+    """The headline end-to-end number, through the reference-facing seam: the
+    UNCHANGED reference Coordinator (baseline/_ref, driven in-process by
+    session3d.Rank3Job) and one GPU worker PROCESS behind its W_* control
+    protocol. Per step: the W_BATCH frame (the step's DAG
+    bytes) goes host -> worker over the wire, the worker enqueues the kernels,
+    and a W_FETCH of one result plane (the worker drains its stream, copies
+    the plane D2H and ships it back) closes the step. None when the reference
+    is not installed."""
+    from paper_2512_19851_b200.launcher import reference_available
+
+    if not reference_available():
+        return None
+    from paper_2512_19851_b200.programs import DagProgram, heat3d_setup, laplace_program, wave2d_setup
+    from paper_2512_19851_b200.session3d import Rank3Job
+    from paper_2512_19851_b200.wire import DTYPE_F32, DTYPE_F64, encode_dag
+
+    prog = DagProgram()
+    n = w["n"]
+    if w["kind"] == "heat3d":
+        arrays = heat3d_setup(prog, n)
+    elif w["kind"] == "wave2d":
+        arrays = wave2d_setup(prog, n, DTYPE_F32)
+    else:
+        laplace_program(prog, n, 0)
+        arrays = (0, 1)
+    shape = prog.shapes[arrays[0]]
+    mid = shape[0] // 2
+    plane = ((mid, mid + 1),) + tuple((0, e) for e in shape[1:])
+    with Rank3Job(1, spares=0) as job:
+        for aid in sorted(prog.shapes):
+            job.create_array(prog.shapes[aid], prog.dtypes.get(aid, DTYPE_F64))
+        job.submit(encode_dag(prog.dag))
+        job.sync()
+        blob = step_dag(w, prog.shapes, prog.dtypes, arrays)
+        for _ in range(max(2, warmup)):
+            job.submit(blob)
+        res = job.fetch(arrays[0], plane)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            job.submit(blob)
+            res = job.fetch(arrays[0], plane)
+        dt = time.perf_counter() - t0
+    return {"value": lup_per_iter(w) * w["iters_per_step"] * steps / dt / 1e9, "unit": "GLUP/s",
+            "h2d_bytes_per_step": len(blob), "d2h_bytes_per_step": int(res.nbytes),
+            "path": "reference Coordinator (baseline/_ref) -> W_BATCH frame -> GPU worker process -> "
+                    "W_FETCH of one result plane (D2H + frame back), per step"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -527,6 +579,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skeleton", default="auto", choices=["auto", "point", "stream"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-seam", action="store_true", help="skip the e2e leg through the worker seam")
     ap.add_argument("--no-check", action="store_true",
                     help="skip the parity check of one bench step against the strict C oracle")
     args = ap.parse_args()
@@ -727,6 +780,12 @@ def main():
     job.close()
     if world == 1 and not args.no_check:
         line["check"] = parity_check(w, args.skeleton)
+    if world == 1 and not args.no_seam:
+        seam = seam_e2e(w, args.steps, args.warmup)
+        if seam is not None:  # the headline e2e is the seam's; the in-process API number stays beside it
+            inproc = line["e2e"]
+            line["e2e"] = dict(seam, in_process={k: inproc[k] for k in ("value", "h2d_bytes_per_step",
+                                                                       "d2h_bytes_per_step", "note")})
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_sample(w)
         line["cpu_baseline"].pop("seconds", None)

@@ -39,7 +39,7 @@ NP = {0: np.float64, 1: np.float32}
 
 class Rank3Job:
     def __init__(self, workers: int, max_workers: int | None = None, odf: int = 1,
-                 ref_path: str = DEFAULT_REF, scratch: str | None = None):
+                 ref_path: str = DEFAULT_REF, scratch: str | None = None, spares: int | None = None):
         if ref_path not in sys.path:
             sys.path.insert(0, ref_path)
         from elastencil.coordinator import Coordinator  # the reference, unmodified
@@ -52,7 +52,7 @@ class Rank3Job:
         self.coord = Coordinator("127.0.0.1:0", workers, self.max_workers, odf, self.scratch)
         self.launcher = GpuLauncher(workers, self.max_workers, odf, scratch=self.scratch,
                                     coordinator_pythonpath=ref_path,
-                                    control_endpoint=self.coord.control_endpoint)
+                                    control_endpoint=self.coord.control_endpoint, spares=spares)
         self.shapes: dict = {}
         self.dtypes: dict = {}
         self._seq = 0

@@ -15,10 +15,18 @@ Every point is computed by the generated expression of codegen._emit_expr
 results are bit-identical to K separate sweeps. Epochs, rounds and launch
 counts are kept per node by the executor.
 
-Kernel structure (one warp-specialised, persistent CTA per SM):
+Kernel structure (one warp-specialised CTA per work item, one resident per SM):
 
 * work item = a BX x BY output column of S over a z-chunk of ZC planes
-  (chunks balanced so every item has the same depth); x tiles start at a
+  (chunks balanced so every item has the same depth; ~96 planes, shorter on
+  small grids so there are >= 2048 items). Items are launched in order, one
+  CTA each: the hardware dispatches the next item to whichever SM frees up,
+  so the ~148 items in flight stay a contiguous band whose neighbours walk z
+  together and share their overlapping halo columns / rows through L2. A
+  persistent grid (CTA b taking items b, b+148, ...) lets CTAs drift apart by
+  tens of planes over a launch and loses that reuse: C4 DRAM reads 12.6 GB vs
+  10.6 GB per launch, 450 vs 525 GLUP/s (profiles/r2_tb_persistent_vs_inorder.md);
+  `persistent=True` keeps the old schedule. x tiles start at a
   16-byte aligned padded column so every thread's V = 16/elem consecutive
   points are one 128-bit vector (fp64 pairs, fp32 quads) in shared memory and
   in HBM;
@@ -26,7 +34,8 @@ Kernel structure (one warp-specialised, persistent CTA per SM):
   (overlapped tiling; m_j rounded up to V) and trails step j-1 by rz planes;
 * producer warp: one elected lane issues one TMA (`cp.async.bulk.tensor.3d`)
   per input plane (tile + halo) into an mbarrier ring (full/empty barriers),
-  running ahead into the next item;
+  `prefetch` planes ahead of the compute window (persistent mode: running
+  ahead into the CTA's next item);
 * compute threads: thread (c, g) owns vector column c and RPT consecutive
   rows of the step-1 frame for every step and every plane. Its z-window of
   every step (2rz+1 planes) lives in registers and rotates by renaming (the
@@ -74,10 +83,11 @@ class TbCfg:
     bx: int = 64            # output columns per item (multiple of 16/elem)
     by: int = 32            # output rows per item
     rpt: int = 2            # consecutive step-1-frame rows per compute thread
-    prefetch: int = 2       # input planes in flight beyond the z window
-    zchunk: int = 192       # target planes per item (chunks are balanced)
+    prefetch: int = 3       # input planes in flight beyond the z window
+    zchunk: int = 96        # target planes per item (chunks are balanced)
+    min_items: int = 2048   # shorter z chunks on small grids until there are this many items
     l2promo: int = 2        # TMA L2 promotion: 0 none, 1 64B, 2 128B, 3 256B
-    persistent: bool = True  # one CTA per SM slot looping over items
+    persistent: bool = False  # one CTA per SM slot looping over items (else one CTA per item)
     hoist: bool = False     # issue every step's shared-memory loads at the top of a plane iteration
 
 
@@ -86,8 +96,9 @@ def _env_cfg() -> TbCfg:
     d = TbCfg()
     return TbCfg(k=int(e("EST_TB_K", d.k)), bx=int(e("EST_TB_BX", d.bx)), by=int(e("EST_TB_BY", d.by)),
                  rpt=int(e("EST_TB_RPT", d.rpt)), prefetch=int(e("EST_TB_PREFETCH", d.prefetch)),
-                 zchunk=int(e("EST_TB_ZCHUNK", d.zchunk)), l2promo=int(e("EST_TB_L2PROMO", d.l2promo)),
-                 persistent=e("EST_TB_PERSISTENT", "1") == "1", hoist=e("EST_TB_HOIST", "0") == "1")
+                 zchunk=int(e("EST_TB_ZCHUNK", d.zchunk)), min_items=int(e("EST_TB_MIN_ITEMS", d.min_items)),
+                 l2promo=int(e("EST_TB_L2PROMO", d.l2promo)),
+                 persistent=e("EST_TB_PERSISTENT", "0") == "1", hoist=e("EST_TB_HOIST", "0") == "1")
 
 
 DEFAULT = _env_cfg()
@@ -527,6 +538,8 @@ def item_geometry(s_lo, s_hi, sm_count: int, lay: dict, xoff: int = 0) -> dict:
     nbx = -(-(s_hi[2] - xt0) // cfg.bx)
     nby = -(-ny // cfg.by)
     nzc = max(1, -(-nz // max(1, cfg.zchunk)))
+    if nbx * nby * nzc < cfg.min_items:  # small grids: more, shorter items (C2 510^3: 32-plane chunks)
+        nzc = max(nzc, min(-(-cfg.min_items // (nbx * nby)), max(1, nz // 16)))
     zc = -(-nz // nzc)
     nzc = -(-nz // zc)
     n_items = nbx * nby * nzc

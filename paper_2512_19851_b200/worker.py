@@ -42,7 +42,8 @@ log = logging.getLogger("elastencil.gpu_worker")
 
 
 class GpuWorker:
-    def __init__(self, worker_id: int, coordinator: str, scratch: str, device: int | None = None):
+    def __init__(self, worker_id: int, coordinator: str, scratch: str, device: int | None = None,
+                 dev=None):
         self.id = worker_id
         self.scratch = scratch
         self.device = gpu_for_slot(worker_id) if device is None else device
@@ -60,9 +61,11 @@ class GpuWorker:
         # CUDA context + libest BEFORE registering: a (re)spawned worker is
         # device-ready when the coordinator's restart stage sees it
         # (coordinator.py:562-579), so W_RESTORE is pure data movement
-        self._dev = None
+        # (a standby spare created its device before it was given an id: `dev`)
+        self._dev = dev
         self._dev_err = None
-        self._dev_thread = threading.Thread(target=self._make_device, daemon=True)
+        self._dev_thread = threading.Thread(target=self._make_device if dev is None else (lambda: None),
+                                            daemon=True)
         self._dev_thread.start()
         self._dev_thread.join()
         self.coord = socket.create_connection((host, int(port)))
@@ -276,17 +279,51 @@ class GpuWorker:
             self.group.close()
 
 
+def standby(device: int):
+    """A warm spare (launcher.GpuLauncher): interpreter, package, libest and
+    the CUDA context on `device` are brought up BEFORE the process has a
+    worker id; it reports READY on stdout and blocks until the launcher's
+    restart stage hands it an id on stdin ("ID <n>"). Context creation
+    (0.6-0.9 s alone, several seconds when eight processes create theirs on
+    one GPU at once; profiles/r1s2_worker_startup.txt) thus leaves the
+    reference rescale's restart stage (coordinator.py:562-579)."""
+    from . import elastic, executor, ipc  # noqa: F401  (warm imports)
+    from .device import Device
+
+    dev = Device(device)
+    dev.sync()
+    sys.stdout.write("READY\n")
+    sys.stdout.flush()
+    line = sys.stdin.readline().split()
+    null = os.open(os.devnull, os.O_WRONLY)  # nobody drains the READY pipe from here on
+    os.dup2(null, 1)
+    os.close(null)
+    if len(line) != 2 or line[0] != "ID":
+        dev.close()
+        return None, None
+    return int(line[1]), dev
+
+
 def worker_main(argv=None) -> int:
-    """`python -m paper_2512_19851_b200.worker --id I --coordinator HOST:PORT --scratch DIR`"""
+    """`python -m paper_2512_19851_b200.worker --id I --coordinator HOST:PORT --scratch DIR`
+    (or `--standby --device G ...`: a warm spare that waits for its id)."""
     import argparse
 
     ap = argparse.ArgumentParser()
-    ap.add_argument("--id", type=int, required=True)
+    ap.add_argument("--id", type=int, default=None)
     ap.add_argument("--coordinator", required=True)
     ap.add_argument("--scratch", required=True)
     ap.add_argument("--device", type=int, default=None)
+    ap.add_argument("--standby", action="store_true")
     args = ap.parse_args(argv)
-    GpuWorker(args.id, args.coordinator, args.scratch, args.device).run()
+    dev = None
+    if args.standby:
+        args.id, dev = standby(args.device or 0)
+        if args.id is None:
+            return 0
+    elif args.id is None:
+        ap.error("--id is required")
+    GpuWorker(args.id, args.coordinator, args.scratch, args.device, dev=dev).run()
     return 0
 
 

@@ -19,7 +19,11 @@ rescale(8), phase 3. Reported:
 
 With one visible GPU all worker processes share it (placement: worker i on
 GPU i mod visible GPUs), so phase rates and stage times include that
-contention; the restart stage is also measured for one worker alone.
+contention; the restart stage is also measured for one worker alone. The
+launcher's warm-spare pool (launcher.GpuLauncher) is waited for before each
+rescale, so the restart stage is the hand-over to standby processes that
+already hold their CUDA context (`restart_handover` records warm / cold);
+EST_SPARES=0 measures cold respawns.
 """
 
 from __future__ import annotations
@@ -67,10 +71,13 @@ def rescaled_run(n: int, iters: int, workers: int, shrink_to: int, fills: int, b
             out["glups"][name] = lups / (time.perf_counter() - t0) / 1e9
 
         phase(f"phase1_{workers}w")
+        spares_ready = job.launcher.wait_spares(300)
         out["rescales"][f"{workers}->{shrink_to}"] = job.rescale(shrink_to)
         phase(f"phase2_{shrink_to}w")
+        spares_ready &= job.launcher.wait_spares(300)
         out["rescales"][f"{shrink_to}->{workers}"] = job.rescale(workers)
         phase(f"phase3_{workers}w")
+        out["restart_handover"] = {"spares_ready": spares_ready, "per_restart": job.launcher.restart_log}
         out["hash"] = {str(a): job.hash(a) for a in sorted(setup.shapes)}
         st = job.stats()
         out["rounds"] = st["rounds"]
@@ -104,7 +111,8 @@ def restart_alone() -> dict:
         job.submit(setup_b)
         job.submit(step_b)
         job.sync()
-        return job.rescale(1)
+        job.launcher.wait_spares(300)
+        return dict(job.rescale(1), handover=job.launcher.restart_log[-1])
 
 
 def main():
@@ -130,7 +138,8 @@ def main():
             "rescales": res["rescales"], "glups": res["glups"],
             "bit_equal_to_unrescaled": res["hash"] == ref,
             "hash_rescaled": res["hash"], "hash_unrescaled": ref,
-            "rounds": res["rounds"], "restart_one_worker_alone": alone}
+            "rounds": res["rounds"], "restart_handover": res.get("restart_handover"),
+            "restart_one_worker_alone": alone}
     print(json.dumps(line), flush=True)
     return 0 if line["bit_equal_to_unrescaled"] else 1
 

@@ -64,6 +64,31 @@ def test_rescale_shrink_then_expand_bit_equal(ref):
     assert len(stats["rescales"]) == 2
 
 
+def test_rescale_hands_over_to_warm_spares(ref):
+    """The restart stage gives worker ids to standby processes that already
+    hold a CUDA context (launcher.GpuLauncher spares): the stage is much
+    shorter than a cold respawn, results stay bit-exact, and the pool refills."""
+    client, programs = ref
+    with GpuLauncher(workers=2, max_workers=2, odf=1) as job:
+        assert job.wait_spares(180), "standby pool did not fill"
+        sess = client.Session(job.client_endpoint)
+        bs = client.BatchingSession(sess, flush_depth=25)
+        try:
+            b = programs.laplace_program(bs, 64, 20)
+            shrink = bs.rescale(1)
+            b = programs.laplace_iteration_statements(bs, b["u"], b["scratch"], 20)
+            assert job.wait_spares(180)
+            expand = bs.rescale(2)
+            b = programs.laplace_iteration_statements(bs, b["u"], b["scratch"], 20)
+            got = bs.fetch(b["u"])
+        finally:
+            sess.shutdown()
+        assert job.restart_log == [{"warm": 1, "cold": 0}, {"warm": 2, "cold": 0}]
+    assert bits_equal(np.asarray(got), laplace_reference(64, 60))
+    print(f"warm restart ms: shrink {shrink.restart_ms:.1f}, expand {expand.restart_ms:.1f}")
+    assert shrink.restart_ms < 500 and expand.restart_ms < 500
+
+
 # ---------------------------------------------------------------------------
 # the reference runtime's behaviours (pkg/tests/test_runtime.py), re-checked
 # with GPU workers and GPU memory daemons behind the unchanged coordinator
@@ -146,7 +171,8 @@ def test_expand_then_immediate_shrink_and_process_census(ref):
         session.rescale(2)
         names = programs.laplace_iteration_statements(session, names["u"], names["scratch"], 7)
         assert bits_equal(np.asarray(session.fetch(names["u"])), laplace_reference(32, 14))
-        pids = job.all_pids()
+        job.wait_spares(180)
+        pids = job.all_pids() + job.spare_pids()  # the standby pool goes down with the job
         s.shutdown()
     finally:
         job.shutdown()
