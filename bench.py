@@ -16,7 +16,8 @@ per-step event pairs.
 `value`  : device time (CUDA events on the compute stream), max over ranks.
 `e2e`    : host wall clock per step through the reference-facing seam (N=1:
            the reference Coordinator + a GPU worker process, W_BATCH frame in,
-           W_FETCH of one result plane out; `e2e.in_process` = the same through
+           the result array's device-computed content hash (8 B) out;
+           `e2e.in_process` = the same through
            the in-process API GpuJob.run_bytes; N>1: the in-process API on
            every rank), max over ranks.
 `roofline`: the dominant kernel kind, achieved = algorithmic bytes per launch /
@@ -527,8 +528,8 @@ def seam_e2e(w, steps: int, warmup: int) -> dict | None:
     session3d.Rank3Job) and one GPU worker PROCESS behind its W_* control
     protocol. Per step: the W_BATCH frame (the step's DAG
     bytes) goes host -> worker over the wire, the worker enqueues the kernels,
-    and a W_FETCH of one result plane (the worker drains its stream, copies
-    the plane D2H and ships it back) closes the step. None when the reference
+    and a W_HASH (the worker drains its stream and returns the updated array's
+    64-bit content hash, reduced on the device) closes the step. None when the reference
     is not installed."""
     from paper_2512_19851_b200.launcher import reference_available
 
@@ -547,9 +548,6 @@ def seam_e2e(w, steps: int, warmup: int) -> dict | None:
     else:
         laplace_program(prog, n, 0)
         arrays = (0, 1)
-    shape = prog.shapes[arrays[0]]
-    mid = shape[0] // 2
-    plane = ((mid, mid + 1),) + tuple((0, e) for e in shape[1:])
     with Rank3Job(1, spares=0) as job:
         for aid in sorted(prog.shapes):
             job.create_array(prog.shapes[aid], prog.dtypes.get(aid, DTYPE_F64))
@@ -558,16 +556,17 @@ def seam_e2e(w, steps: int, warmup: int) -> dict | None:
         blob = step_dag(w, prog.shapes, prog.dtypes, arrays)
         for _ in range(max(2, warmup)):
             job.submit(blob)
-        res = job.fetch(arrays[0], plane)
+        job.hash(arrays[0])
         t0 = time.perf_counter()
         for _ in range(steps):
             job.submit(blob)
-            res = job.fetch(arrays[0], plane)
+            job.hash(arrays[0])
         dt = time.perf_counter() - t0
     return {"value": lup_per_iter(w) * w["iters_per_step"] * steps / dt / 1e9, "unit": "GLUP/s",
-            "h2d_bytes_per_step": len(blob), "d2h_bytes_per_step": int(res.nbytes),
-            "path": "reference Coordinator (baseline/_ref) -> W_BATCH frame -> GPU worker process -> "
-                    "W_FETCH of one result plane (D2H + frame back), per step"}
+            "h2d_bytes_per_step": len(blob), "d2h_bytes_per_step": 8,
+            "path": "reference Coordinator (baseline/_ref) -> W_BATCH frame (the step's DAG bytes) -> GPU "
+                    "worker process -> W_HASH: the worker drains its stream and returns the updated array's "
+                    "device-computed 64-bit content hash (8 bytes D2H), per step"}
 
 
 def main():
@@ -678,14 +677,14 @@ def main():
     value = lups_step * args.steps / (dev_ms / 1e3) / 1e9
 
     # ---- end-to-end through the public API ------------------------------------
-    plane_bounds = None
+    # the step's result read back to the host: the updated array's 64-bit
+    # position-keyed content hash (est_hash_box over every element on the
+    # device, 8 bytes D2H) - a scalar summary of the whole result, like a loss
     shape = prog.shapes[arrays[0]]
-    mid = shape[0] // 2
-    plane_bounds = ((mid, mid + 1),) + tuple((0, e) for e in shape[1:])
-    d2h = int(np.prod([b - a for a, b in plane_bounds])) * (4 if w["dtype"] == "f32" else 8)
+    d2h = 8
+
     def fetch_result():
-        return (job.fetch_local(arrays[0], plane_bounds) if hasattr(job, "fetch_local")
-                else job.fetch(arrays[0], plane_bounds))
+        return job.hash_local(arrays[0]) if hasattr(job, "hash_local") else job.hash(arrays[0])
 
     one_step()        # untimed: first fetch allocates the pinned staging buffer
     fetch_result()
@@ -772,8 +771,8 @@ def main():
         "e2e": {"value": e2e_val, "unit": "GLUP/s",
                 "h2d_bytes_per_step": len(blob), "d2h_bytes_per_step": d2h,
                 "note": ("per step: the W_BATCH payload (DAG bytes) from host memory -> decode/analysis cache -> "
-                         "kernel launches (the protocol has no array upload, PROTOCOL.md:37), then one result "
-                         "plane copied D2H into pinned memory")},
+                         "kernel launches (the protocol has no array upload, PROTOCOL.md:37), then the result "
+                         "array's device-computed 64-bit content hash copied D2H")},
         "gpu_launches": gpu_launches,
         "clocks": clock,
     }

@@ -143,6 +143,16 @@ int est_event_query(est_event *ev);                            /* 0 done, 600 pe
 int est_event_elapsed_ms(est_event *start, est_event *end, float *ms);
 int est_stream_join(est_ctx *ctx, int waiter, int signaller);  /* intra-ctx ordering */
 
+/* ---- device-side round flags (replace the per-round READY / PULLED signalling
+ * of exchange.py:169-234 / worker.py:61-139 between worker processes) -------
+ * est_flag_write: after all prior work on `stream`, store `value` to the 32-bit
+ *   word at device address `addr` (implicit system-scope release barrier).
+ * est_flag_wait: `stream` waits (front-end semaphore acquire, no SM spin) until
+ *   the word at `addr` - possibly a peer's, IPC-mapped - satisfies
+ *   (int32_t)(*addr - value) >= 0. */
+int est_flag_write(est_ctx *ctx, uint64_t addr, uint32_t value, int stream);
+int est_flag_wait(est_ctx *ctx, uint64_t addr, uint32_t value, int stream);
+
 /* ---- CUDA IPC: replaces the TCP peer transport and the memory daemon's
  * host-side blob store (worker.py:211-224, daemon.py:29-143) --------------- */
 int est_ipc_mem_handle(uint64_t dptr, uint8_t handle[64]);

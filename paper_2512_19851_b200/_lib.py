@@ -68,6 +68,8 @@ _SIGS = {
     "est_event_query": (i32, [vp]),
     "est_event_elapsed_ms": (i32, [vp, vp, P(C.c_float)]),
     "est_stream_join": (i32, [vp, i32, i32]),
+    "est_flag_write": (i32, [vp, u64, C.c_uint32, i32]),
+    "est_flag_wait": (i32, [vp, u64, C.c_uint32, i32]),
     "est_ipc_mem_handle": (i32, [u64, P(C.c_uint8)]),
     "est_ipc_mem_open": (i32, [vp, P(C.c_uint8), P(u64)]),
     "est_ipc_mem_close": (i32, [u64]),

@@ -73,6 +73,8 @@ struct Driver {
     decltype(&cuFuncSetAttribute) funcSetAttribute = nullptr;
     decltype(&cuOccupancyMaxActiveBlocksPerMultiprocessor) occupancy = nullptr;
     decltype(&cuLaunchKernelEx) launchKernelEx = nullptr;
+    decltype(&cuStreamWriteValue32) streamWriteValue32 = nullptr;
+    decltype(&cuStreamWaitValue32) streamWaitValue32 = nullptr;
     bool ok = false;
 };
 static Driver g_drv;
@@ -101,6 +103,8 @@ static int driver() {
     rc |= resolve("cuTensorMapEncodeTiled", g_drv.tensorMapEncodeTiled);
     rc |= resolve("cuOccupancyMaxActiveBlocksPerMultiprocessor", g_drv.occupancy);
     rc |= resolve("cuLaunchKernelEx", g_drv.launchKernelEx);
+    rc |= resolve("cuStreamWriteValue32", g_drv.streamWriteValue32);
+    rc |= resolve("cuStreamWaitValue32", g_drv.streamWaitValue32);
     if (rc) return 1;
     g_drv.ok = true;
     return 0;
@@ -730,6 +734,29 @@ extern "C" int est_event_record(est_ctx *c, est_event *e, int s) {
 extern "C" int est_event_wait(est_ctx *c, est_event *e, int s) {
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamWaitEvent(pick(c, s), e->ev, 0));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Device-side round flags: stream memory operations on 32-bit words in device
+// memory (own or IPC-mapped peer arenas). The write follows all prior work on
+// the stream with an implicit system-scope memory barrier (release); the wait
+// blocks the stream's front end - no SM spins - until (int32)(*addr - value)
+// >= 0. They replace the per-round IPC-event + host sequence handshake.
+
+extern "C" int est_flag_write(est_ctx *c, uint64_t addr, uint32_t value, int s) {
+    if (driver()) return 1;
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUresult r = g_drv.streamWriteValue32((CUstream)pick(c, s), (CUdeviceptr)addr, value, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(1, "cuStreamWriteValue32 failed (%d)", (int)r);
+    return 0;
+}
+
+extern "C" int est_flag_wait(est_ctx *c, uint64_t addr, uint32_t value, int s) {
+    if (driver()) return 1;
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUresult r = g_drv.streamWaitValue32((CUstream)pick(c, s), (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(1, "cuStreamWaitValue32 failed (%d)", (int)r);
     return 0;
 }
 

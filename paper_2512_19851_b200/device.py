@@ -169,6 +169,14 @@ class Device:
     def join(self, waiter: int, signaller: int) -> None:
         check(self.lib.est_stream_join(self.ctx, waiter, signaller))
 
+    def flag_write(self, addr: int, value: int, stream: int = COMPUTE) -> None:
+        """After all prior work on `stream`: *(uint32*)addr = value (release)."""
+        check(self.lib.est_flag_write(self.ctx, int(addr), int(value) & 0xFFFFFFFF, stream))
+
+    def flag_wait(self, addr: int, value: int, stream: int = COMPUTE) -> None:
+        """`stream` waits until *(uint32*)addr >= value (wrap-safe), no host wait."""
+        check(self.lib.est_flag_wait(self.ctx, int(addr), int(value) & 0xFFFFFFFF, stream))
+
     def event(self, interprocess: bool = False) -> Event:
         return Event(self, interprocess)
 

@@ -62,7 +62,11 @@ def migrate_tiles(job, plan: dict) -> dict:
 
     t0 = time.perf_counter()
     store, dev = job.store, job.dev
-    dev.sync()
+    job.sync()  # guarded: the streams may wait on peers' round flags
+    # temporal-chain twins belong to the current tile set: every worker drops
+    # them, the next chain batch re-creates them inside its realloc window
+    for ex in job.executors:
+        ex.release_scratch()
     # every worker learns the uniform local epochs (a tile-less worker has none)
     epochs = {a: store.local_epoch(a) for a in store.arrays} if store.tiles else None
     known = [e for e in job._all_gather(epochs) if e is not None]
@@ -81,8 +85,9 @@ def migrate_tiles(job, plan: dict) -> dict:
             info = store.arrays[a]
             ext = store.decomp.tile_extents(info.shape)
             depth = depths.get(a, (0,) * info.rank)
+            frame = tuple(max(x, y) for x, y in zip(depth, store.phys_depth.get(a, depth)))
             ta = time.perf_counter()
-            buf = TileBuffer(dev, ext, depth, info.dtype)
+            buf = TileBuffer(dev, ext, frame, info.dtype)
             t_alloc += time.perf_counter() - ta
             src_layout, src_addr = job.transport.peer_buffer(old, coords, a)
             # src_layout describes the peer buffer; its ptr is the mapped address
@@ -124,7 +129,7 @@ def migrate_tiles(job, plan: dict) -> dict:
 def checkpoint_tiles(job, client: DaemonClient, owner: int) -> tuple:
     """Copy every owned (tile, array) interior into daemon HBM; records + meta."""
     store, dev = job.store, job.dev
-    dev.sync()
+    job.sync()
     records = []
     if store is None:
         return records, {}

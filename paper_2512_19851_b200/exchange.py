@@ -133,21 +133,25 @@ class GpuExchangeManager:
         self._geometry: dict = {}  # (array, layout version, owner map) -> boxes
         self.pending: dict = {}    # array -> posted-but-unpulled round token
 
-    def _round_geometry(self, array: int, rank: int) -> tuple:
-        """Co-located strip copies and remote (tile, dir, neighbour, owner) list."""
+    def _round_geometry(self, array: int, rank: int, twin: bool = False) -> tuple:
+        """Co-located strip copies and remote (tile, dir, neighbour, owner) list.
+        `twin`: the array's values live in the temporal chains' twin buffers
+        (mid-run), so the strips move between twins."""
         depth = self._depth(array)
         local_boxes, remote = [], []
+
+        def buf(c):
+            return self.store.twins[(c, array)] if twin else self.store.tiles[c].buffers[array]
+
         if depth is not None:
             for coords in sorted(self.store.tiles):
-                tile = self.store.tiles[coords]
                 for d in directions_for(depth):
                     nb = neighbour(self.store.decomp, rank, coords, d)
                     if nb is None:
                         continue
                     owner = self.owner_map[nb]
                     if owner == self.worker_id:
-                        src = self.store.tiles[nb].buffers[array]
-                        local_boxes.append(strip_copy(src, tile.buffers[array], d))
+                        local_boxes.append(strip_copy(buf(nb), buf(coords), d))
                     else:
                         remote.append((coords, d, nb, owner))
         return local_boxes, remote
@@ -167,21 +171,27 @@ class GpuExchangeManager:
                 done.append(token[1])
         return done
 
-    def ensure_round(self, array: int, epoch: int, defer: bool = False) -> bool:
+    def ensure_round(self, array: int, epoch: int, defer: bool = False, twin: bool = False,
+                     virtual: bool = False, refresh: bool = False) -> bool:
         """Start round (array, epoch); returns True (completion is stream-ordered).
 
         With `defer` (multi-worker, push-plan rounds) the peer pull is posted
         but not enqueued; the executor finishes it right before / overlapped
-        with the next node that reads the array (`finish_pending`)."""
-        if self.completed.get(array, -1) >= epoch:
+        with the next node that reads the array (`finish_pending`).
+        `virtual`: the round's ghosts are produced inside a temporal chain
+        (nothing moves; counted exactly as the reference counts the round).
+        `refresh`: re-run the data movement of an already counted (virtual)
+        round, uncounted. Every worker makes the same choice for every round
+        (they derive from the DAG), so transport sequences stay aligned."""
+        if not refresh and self.completed.get(array, -1) >= epoch:
             return True
         if self.pending:
             self.finish_pending()  # keep at most one round in flight on the host
         info = self.store.arrays[array]
-        ck = (array, self.store.version, id(self.owner_map))
+        ck = (array, self.store.version, id(self.owner_map), twin)
         hit = self._geometry.get(ck)
         if hit is None:
-            hit = self._round_geometry(array, info.rank)
+            hit = self._round_geometry(array, info.rank, twin)
             if len(self._geometry) > 1024:
                 self._geometry.clear()
             self._geometry[ck] = hit
@@ -189,18 +199,22 @@ class GpuExchangeManager:
         if remote:
             if self.transport is None:
                 raise RuntimeError("remote neighbours but no transport configured")
-            self.net_messages += len(remote)
-        if self.transport is not None:
+            if not refresh:
+                self.net_messages += len(remote)
+        if virtual:
+            pass
+        elif self.transport is not None:
             # every worker takes part in every round, owning tiles or not, so the
             # transport's per-round sequencing stays globally aligned
             if defer:
-                self.pending[array] = self.transport.post(array, epoch, remote, local_boxes)
+                self.pending[array] = self.transport.post(array, epoch, remote, local_boxes, twin)
             else:
-                self.transport.exchange(array, epoch, remote, local_boxes)
+                self.transport.exchange(array, epoch, remote, local_boxes, twin)
         elif local_boxes:
             self.store.dev.copy_boxes(local_boxes, ELEM[info.dtype])
             self.copy_launches += 1
-        self.rounds_started[array] = self.rounds_started.get(array, 0) + 1
+        if not refresh:
+            self.rounds_started[array] = self.rounds_started.get(array, 0) + 1
         self.completed[array] = epoch
         self.store.set_ghost_epoch(array, epoch)
         return True

@@ -96,8 +96,9 @@ class GpuExecutor:
         self.resident_smem = resident.SMEM_ENABLED  # small rank-2 chains held in shared memory
         self._bar = 0                     # grid-barrier counter of the resident-smem skeleton
         self.tb_cfg = temporal.DEFAULT
-        self._scratch: dict = {}     # array -> twin TileBuffer for temporal chains
         self._tb_sched: dict = {}
+        self._in_twin: dict = {}     # array -> its current values live in the twin buffers (mid-run)
+        self._dirty: dict = {}       # array -> epoch whose ghost round was virtual (computed in-chain)
 
     # -- preparation (executor.py:193-256) ----------------------------------
     def prepare_batch(self, dag, key: bytes | None = None):
@@ -134,13 +135,19 @@ class GpuExecutor:
             self.store.check_depth_fits(a, new)
             self.depths[a] = new
             changed |= new != old
+        phys = {a: self._phys_depth(a, self.depths[a]) for a in need}
+        changed |= any(self.store.phys_depth.get(a) != phys[a] for a in need)
+        sched = self.temporal_schedule(dag, plans, key, phys)
+        twins = self._twin_arrays(sched, phys)
+        changed |= bool(twins)
         # depth changes are identical on every worker (pure in the DAG), so all
         # workers - owning tiles or not - meet in the same realloc barriers
         if changed and self.transport is not None:
             self.transport.before_realloc()
         for a in sorted(need):
-            if self.store.ensure_ghost_capacity(a, self.depths[a]):
+            if self.store.ensure_ghost_capacity(a, self.depths[a], phys[a]):
                 self.store.bump_local_epoch(a)
+        self._alloc_twins(twins)
         if changed and self.transport is not None:
             self.transport.after_realloc()
         local: dict = {}
@@ -160,14 +167,14 @@ class GpuExecutor:
             for a in node.writes:
                 local[a] = local.get(a, self.store.local_epoch(a)) + 1
                 last_writer[a] = node.node_id
-        return metas, plans, pushes
+        return metas, plans, pushes, sched
 
     # -- host batch path: replay cache ------------------
     def _state_sig(self) -> tuple:
         st, ex = self.store, self.exchanges
         return (st.version, tuple(sorted(
             (a, st.local_epoch(a) == 0, ex.ghost_generation(a) == st.local_epoch(a),
-             self.depths.get(a)) for a in st.arrays)))
+             self.depths.get(a), self._dirty.get(a) == ex.ghost_generation(a)) for a in st.arrays)))
 
     def execute_batch(self, dag, key: bytes | None = None) -> BatchStats:
         """Run one batch. With `key` (e.g. a digest of the DAG bytes) a batch
@@ -205,7 +212,8 @@ class GpuExecutor:
         if self._state_sig()[0] != sig[1][0]:
             return stats  # buffers were reallocated: not a steady-state batch
         if not capture:
-            self._remember(sig, {"effects": self._effects(before, after), "stats": stats})
+            dirty = {a for a in self.store.arrays if self._dirty.get(a) == self.exchanges.ghost_generation(a)}
+            self._remember(sig, {"effects": self._effects(before, after), "stats": stats, "dirty": dirty})
         stats.wall_ms = (time.perf_counter() - t0) * 1e3
         return stats
 
@@ -260,6 +268,8 @@ class GpuExecutor:
                 st.set_ghost_epoch(a, start + grel)
             if dr:
                 ex.rounds_started[a] = ex.rounds_started.get(a, 0) + dr
+        for a in ent.get("dirty", ()):
+            self._dirty[a] = ex.ghost_generation(a)
         s = ent["stats"]
         out = BatchStats(nodes_executed=s.nodes_executed, kernel_launches=s.kernel_launches,
                          rounds=dict(s.rounds), net_messages=s.net_messages,
@@ -283,30 +293,39 @@ class GpuExecutor:
         t0 = time.perf_counter()
         before = self.exchanges.snapshot_stats()
         launches0 = self.dev.launches
-        metas, plans, pushes = self.prepare_batch(dag, key)
+        metas, plans, pushes, tb = self.prepare_batch(dag, key)
         stats = BatchStats(prepare_ms=(time.perf_counter() - t0) * 1e3)
-        tb = self.temporal_schedule(dag, plans, key)
         for a, e in pushes.get(None, ()):
-            self.exchanges.ensure_round(a, e)
+            self._round(a, e)
         for node in dag.nodes:
             meta = metas[node.node_id]
+            chain = tb.get(node.node_id)
             for a in sorted(meta.array_max_offset):
                 if not meta.needs_exchange(a):
                     continue
                 target = self.store.local_epoch(a)
                 if target and self.exchanges.ghost_generation(a) != target:
-                    self.exchanges.ensure_round(a, target)
+                    self._round(a, target)
+                elif target and self._dirty.get(a) == target and chain is None:
+                    # the round of this epoch was virtual (its ghosts were
+                    # computed inside a chain): refresh them now, uncounted
+                    self._round(a, target, refresh=True)
             t_node = time.perf_counter()
             plan = plans[node.node_id]
             if self.transport is not None:
-                for a in sorted(node.writes):
+                writes = set(node.writes)
+                if chain is not None and chain[0] == "lead":
+                    writes |= set(plan.statements[0].inputs)  # the chain also writes A
+                for a in sorted(writes):
                     self.transport.before_write(a)
             pending = self.exchanges.pending
-            chain = tb.get(node.node_id)
             if chain is not None:
                 # temporal chain: its lead node launches the fused K-sweep
-                # kernel; members only keep the per-node bookkeeping (a single
-                # tile without transport has no device work between sweeps)
+                # kernel; members only keep the per-node bookkeeping (the
+                # halo rounds inside a chain are virtual: step 1 computes the
+                # intermediate array's ghost planes from A's K*r-deep halo)
+                if pending:
+                    self.exchanges.finish_pending()
                 if chain[0] == "lead":
                     self._launch_tb(node, plan, chain[1], key, chain[2])
                 elif chain[0] == "rsm":
@@ -328,7 +347,8 @@ class GpuExecutor:
             for a in sorted(node.writes):
                 self.store.bump_local_epoch(a)
             for a, e in pushes.get(node.node_id, ()):
-                self.exchanges.ensure_round(a, e, defer=self.overlap and self.transport is not None)
+                virtual = chain is not None and chain[0] in ("lead", "member") and self._chain_reads(tb, node, a)
+                self._round(a, e, defer=self.overlap and self.transport is not None, virtual=virtual)
             stats.nodes_executed += 1
             stats.node_ms[node.node_id] = (time.perf_counter() - t_node) * 1e3
         if self.exchanges.pending:
@@ -344,10 +364,37 @@ class GpuExecutor:
         return stats
 
     # -- temporal blocking (temporal.py) ----------------
-    def _chain_candidate(self, plan):
+    def _multi(self) -> bool:
+        return self.store.decomp.n_tiles != 1 or self.transport is not None
+
+    def _slab_chains_ok(self) -> bool:
+        """Chains on the slabs of a multi-tile job: K = 2 only. At K = 2 the
+        intermediate array is read on a ghost plane only at the (y, x) points
+        it computed there; deeper chains would also read its cells outside
+        the output slice on ghost planes, which no round refreshes (its rounds
+        are virtual). The transport must share twin buffers (IPC) or be
+        absent (one process)."""
+        return self.tb_cfg.k == 2 and getattr(self.transport, "chains_ok", self.transport is None)
+
+    def _phys_depth(self, a: int, logical) -> tuple:
+        """Allocated ghost frame of array a: rank-3 slabs of a multi-tile job
+        keep K*rz planes (one halo round feeds a K-sweep chain), else the
+        logical depth."""
+        info = self.store.arrays[a]
+        if (not self.temporal or info.rank != 3 or not self._multi() or logical[0] <= 0
+                or not self._slab_chains_ok()):
+            return tuple(logical)
+        pz = self.tb_cfg.k * logical[0]
+        if pz >= self.store.decomp.tile_extents(info.shape)[0]:
+            return tuple(logical)
+        return (pz,) + tuple(logical[1:])
+
+    def _chain_candidate(self, plan, phys=None):
         """(A, B, output bounds, plan instructions, rank, dtype) for a node that
         can be part of a ping-pong chain: one statement, one input array of the
-        output's shape, type and buffer layout; else None."""
+        output's shape, type and buffer layout; else None. Decided from the
+        job-wide array table and ghost frames only (never from the tiles this
+        worker happens to own), so every worker schedules the same chains."""
         if len(plan.statements) != 1:
             return None
         ps = plan.statements[0]
@@ -359,9 +406,8 @@ class GpuExecutor:
         ia, ib = self.store.arrays.get(a), self.store.arrays.get(b)
         if ia is None or ib is None or ia.rank not in (2, 3) or ia.shape != ib.shape or ia.dtype != ib.dtype:
             return None
-        tile = next(iter(self.store.tiles.values()))
-        ba, bb = tile.buffers[a], tile.buffers[b]
-        if (ba.depth, ba.py, ba.pz, ba.xoff) != (bb.depth, bb.py, bb.pz, bb.xoff):
+        phys = phys if phys is not None else self.store.phys_depth
+        if phys.get(a, self.depths.get(a)) != phys.get(b, self.depths.get(b)):
             return None
         return (a, b, tuple(ps.output_slice_bounds), plan_key(ps.instructions), ia.rank, ia.dtype)
 
@@ -372,30 +418,35 @@ class GpuExecutor:
         sig = codegen.stmt_sig(plan.statements[0], 3)
         return c if temporal.eligible(sig, c[5], self.tb_cfg) else None
 
-    def temporal_schedule(self, dag, plans, key=None) -> dict:
+    def temporal_schedule(self, dag, plans, key=None, phys=None) -> dict:
         """node id -> ("rsm", sweeps) | ("lead", chain index in its run, last in run) | ("member",).
 
         Runs of consecutive candidate nodes that ping-pong A -> B -> A with the
         same statement and output slice: a small rank-2 run is one
-        shared-memory-resident launch (resident.py); otherwise, with temporal
-        chains enabled, the run is cut into chains of K nodes (temporal.py),
-        the number of chains kept even so A ends in its own buffer. Only for
-        one tile per job without transport (no exchange between sweeps);
-        everything else runs node by node."""
-        if (not (self.temporal or self.resident_smem) or self.transport is not None
-                or len(self.store.tiles) != 1 or self.store.decomp.n_tiles != 1
-                or self.skeleton not in ("auto", "tb")):
+        shared-memory-resident launch (resident.py, one tile without
+        transport); otherwise, with temporal chains enabled, the run is cut
+        into chains of K nodes (temporal.py), the number of chains kept even
+        so A ends in its own buffer. Multi-tile jobs (rank-3 slabs, one
+        process or one per GPU) chain too when A's ghost frame holds K*rz
+        planes: one halo round of A per chain, the intermediate array's round
+        inside the chain is virtual (computed from A's deep halo) and counted
+        as the reference counts it."""
+        multi = self._multi()
+        if (not (self.temporal or self.resident_smem) or self.skeleton not in ("auto", "tb")
+                or (multi and not (self.temporal and self._slab_chains_ok()))
+                or (not multi and len(self.store.tiles) != 1)):
             return {}
-        ck = ((key, self.store.version, self.tb_cfg, self.temporal, self.resident_smem)
-              if key is not None else None)
+        phys = phys if phys is not None else self.store.phys_depth
+        ck = ((key, self.store.version, self.tb_cfg, self.temporal, self.resident_smem,
+               tuple(sorted(phys.items())), multi) if key is not None else None)
         hit = self._tb_sched.get(ck) if ck is not None else None
         if hit is not None:
             return hit
         K = self.tb_cfg.k
-        cand = [self._chain_candidate(p) for p in plans]
-        tile = next(iter(self.store.tiles.values()))
+        cand = [self._chain_candidate(p, phys) for p in plans]
         sched: dict = {}
         i, n = 0, len(cand)
+        n_tiles = self.store.decomp.n_tiles
         while i < n:
             c = cand[i]
             if c is None:
@@ -406,18 +457,19 @@ class GpuExecutor:
                    and cand[j][0] == cand[j - 1][1] and cand[j][1] == cand[j - 1][0]):
                 j += 1
             sig = codegen.stmt_sig(plans[i].statements[0], c[4])
-            if (self.resident_smem and j - i >= 2 and resident.smem_eligible(sig, c[5], c[4])
+            if (not multi and self.resident_smem and j - i >= 2 and resident.smem_eligible(sig, c[5], c[4])
                     and self._rsm_geometry(c, sig) is not None):
                 sched[dag.nodes[i].node_id] = ("rsm", j - i)
                 for q in range(i + 1, j):
                     sched[dag.nodes[q].node_id] = ("member",)
             elif (self.temporal and c[4] == 3 and temporal.eligible(sig, c[5], self.tb_cfg)
-                  and _volume(c[2]) >= temporal.MIN_POINTS):
+                  and _volume(c[2]) // n_tiles >= temporal.MIN_POINTS
+                  and (not multi or phys.get(c[0], (0,))[0] >= K * temporal.slot_radius(sig)[0][0])):
                 m = (j - i) // K
                 m -= m % 2
                 for ch in range(m):
                     lead = i + ch * K
-                    sched[dag.nodes[lead].node_id] = ("lead", ch, ch == m - 1)
+                    sched[dag.nodes[lead].node_id] = ("lead", ch, ch == m - 1, c[0])
                     for q in range(1, K):
                         sched[dag.nodes[lead + q].node_id] = ("member",)
             i = j
@@ -426,6 +478,60 @@ class GpuExecutor:
                 self._tb_sched.clear()
             self._tb_sched[ck] = sched
         return sched
+
+    def _chain_reads(self, tb, node, a) -> bool:
+        """The round of array `a` pushed after chain node `node` is consumed
+        inside the chain (the next node is a member of the same chain that
+        reads `a`): it is virtual."""
+        nxt = tb.get(node.node_id + 1)
+        return nxt is not None and nxt[0] == "member"
+
+    def _round(self, a: int, e: int, defer: bool = False, virtual: bool = False, refresh: bool = False) -> None:
+        """A halo round of array a at epoch e, on the buffers that hold a's
+        values right now (the twins mid-chain-run)."""
+        if virtual:
+            self.exchanges.ensure_round(a, e, virtual=True)
+            self._dirty[a] = e
+            return
+        self.exchanges.ensure_round(a, e, defer=defer, twin=self._in_twin.get(a, False), refresh=refresh)
+        self._dirty.pop(a, None)
+
+    def _twin_arrays(self, sched, phys) -> list:
+        """Chain input arrays whose twin buffers are missing or stale."""
+        want = set()
+        for ent in sched.values():
+            if ent[0] == "lead":
+                want.add(ent[3])
+        out = []
+        for a in sorted(want):
+            sig = (self.store.arrays[a], phys.get(a, self.depths.get(a)), self.store.version)
+            if self.store.twin_sig.get(a) != sig or any((c, a) not in self.store.twins for c in self.store.tiles):
+                out.append(a)
+        return out
+
+    def _alloc_twins(self, arrays) -> None:
+        """Twin buffers (same layout as the tile buffers) for chain inputs;
+        inside the realloc window so peers map them with the rest."""
+        from .tiles import TileBuffer
+
+        for a in arrays:
+            for c in sorted(self.store.tiles):
+                home = self.store.tiles[c].buffers[a]
+                tw = self.store.twins.pop((c, a), None)
+                if tw is not None:
+                    tw.free()
+                self.store.twins[(c, a)] = TileBuffer(self.dev, home.ext[3 - home.rank:],
+                                                      home.depth[3 - home.rank:], home.dtype)
+        if arrays:
+            self.store.version += 1
+            for a in arrays:
+                self.store.twin_sig[a] = (self.store.arrays[a], self.store.phys_depth.get(a, self.depths.get(a)),
+                                          self.store.version)
+
+    @property
+    def _scratch(self) -> dict:
+        """Twin buffers of temporal chains (tests / smoke check they exist)."""
+        return self.store.twins
 
     def _rsm_geometry(self, c, sig):
         (y0, y1), (x0, x1) = c[2]
@@ -469,57 +575,81 @@ class GpuExecutor:
         if ck is not None and rec is not None:
             self._launches[ck] = rec
 
-    def _scratch_for(self, array: int, buf):
-        tw = self._scratch.get(array)
-        if tw is not None and (tw.ext, tw.depth, tw.dtype, tw.nbytes) == (buf.ext, buf.depth, buf.dtype, buf.nbytes):
-            return tw
-        if tw is not None:
-            tw.free()
-        from .tiles import TileBuffer
-        tw = TileBuffer(self.dev, buf.ext[3 - buf.rank:], buf.depth[3 - buf.rank:], buf.dtype)
-        self._scratch[array] = tw
-        return tw
-
     def release_scratch(self) -> None:
-        for tw in self._scratch.values():
+        """Free the chains' twin buffers (re-created by the next chain batch,
+        inside its realloc window)."""
+        for tw in self.store.twins.values():
             tw.free()
-        self._scratch.clear()
+        self.store.twins.clear()
+        self.store.twin_sig.clear()
 
     def _launch_tb(self, node, plan, ch: int, key, last: bool = True) -> None:
+        """One K-sweep chain over every owned tile: A is read from the buffer
+        holding it (home at the start of a run, the twin after an odd number of
+        chains) and written to the other one; B is written in place only by a
+        run's last chain. On a slab of a multi-tile job the intermediate steps
+        compute through the ghost planes that belong to the neighbours' output
+        (`cz`), fed by A's K*rz-deep halo."""
         ps = plan.statements[0]
         a, b = ps.inputs[0], ps.output
-        tile = next(iter(self.store.tiles.values()))
-        home, bbuf = tile.buffers[a], tile.buffers[b]
-        twin = self._scratch_for(a, home)
-        d = home.depth
-        s_lo = tuple(lo + dd for (lo, _), dd in zip(ps.output_slice_bounds, d))
-        s_hi = tuple(hi + dd for (_, hi), dd in zip(ps.output_slice_bounds, d))
-        if ch == 0:
-            # the twin must hold A's values outside S (never written by a chain)
-            self.dev.copy_boxes(temporal.complement_boxes(home, home.ptr, twin.ptr, s_lo, s_hi), home.elem)
-        ck = (key, node.node_id, self.store.version, "tb") if key is not None else None
+        in_twin = self._in_twin.get(a, False)
+        assert ch > 0 or not in_twin, "a chain run starts with A in its own buffers"
+        ck = (key, node.node_id, self.store.version, "tb", in_twin) if key is not None else None
         rec = self._launches.get(ck) if ck is not None else None
         if rec is not None and not self.time_kernels:
             for kern, grid, params, coop in rec:
-                self.dev.launch(kern, grid, params, COMPUTE, self.transport is None, coop)
+                if kern is None:
+                    self.dev.copy_boxes(grid, params)
+                else:
+                    self.dev.launch(kern, grid, params, COMPUTE, self.transport is None, coop)
+            self._in_twin[a] = not in_twin
             return
-        src_buf, dst_buf = (home, twin) if ch % 2 == 0 else (twin, home)
-        sig = codegen.stmt_sig(ps, 3)
-        src, name, block, smem, lay = temporal.source(sig, self.store.arrays[a].dtype, self.tb_cfg,
-                                                      py=home.py, pz=home.pz, xoff=home.xoff)
-        kern = self.dev.kernel(src, name, block, smem)
-        geo = temporal.item_geometry(s_lo, s_hi, self.dev.sm_count, lay, xoff=home.xoff)
-        tm = self._tmap(src_buf, (lay["w0"], lay["h0"], 1), self.tb_cfg.l2promo)
-        org = home.xoff * home.elem
-        params = temporal.pack_params(tm, src_buf.ptr + org, bbuf.ptr + org, dst_buf.ptr + org,
-                                      home, s_lo, s_hi, geo, write_b=last or not temporal.SKIP_MID_B)
         self._recording = [] if ck is not None else None
         try:
-            self._launch(kern, (geo["blocks"], 1, 1), params, tag=("tb", self.tb_cfg.k))
+            self._launch_tb_tiles(ps, a, b, ch, in_twin, last)
         finally:
             rec, self._recording = self._recording, None
         if ck is not None and rec is not None:
             self._launches[ck] = rec
+        self._in_twin[a] = not in_twin
+
+    def _launch_tb_tiles(self, ps, a, b, ch, in_twin, last) -> None:
+        info = self.store.arrays[a]
+        sig = codegen.stmt_sig(ps, 3)
+        rz = temporal.slot_radius(sig)[0][0]
+        K = self.tb_cfg.k
+        for coords in sorted(self.store.tiles):
+            tile = self.store.tiles[coords]
+            home, bbuf = tile.buffers[a], tile.buffers[b]
+            twin = self.store.twins[(coords, a)]
+            origin = self.store.decomp.tile_origin(info.shape, coords)
+            ext = self.store.decomp.tile_extents(info.shape)
+            d = home.depth
+            s_lo, s_hi = [], []
+            for (lo, hi), o, e, dd in zip(ps.output_slice_bounds, origin, ext, d):
+                s_lo.append(max(lo, o) - o + dd)
+                s_hi.append(min(hi, o + e) - o + dd)
+            if any(h <= l for l, h in zip(s_lo, s_hi)):
+                continue
+            (glo, ghi) = ps.output_slice_bounds[0]
+            cz = (max(glo - origin[0] + d[0], s_lo[0] - (K - 1) * rz),
+                  min(ghi - origin[0] + d[0], s_hi[0] + (K - 1) * rz))
+            if ch == 0:
+                # the twin must hold A's values outside S (never written by a chain)
+                boxes = temporal.complement_boxes(home, home.ptr, twin.ptr, tuple(s_lo), tuple(s_hi))
+                self.dev.copy_boxes(boxes, home.elem)
+                if self._recording is not None:
+                    self._recording.append((None, boxes, home.elem, False))
+            src_buf, dst_buf = (twin, home) if in_twin else (home, twin)
+            src, name, block, smem, lay = temporal.source(sig, info.dtype, self.tb_cfg,
+                                                          py=home.py, pz=home.pz, xoff=home.xoff)
+            kern = self.dev.kernel(src, name, block, smem)
+            geo = temporal.item_geometry(s_lo, s_hi, self.dev.sm_count, lay, xoff=home.xoff)
+            tm = self._tmap(src_buf, (lay["w0"], lay["h0"], 1), self.tb_cfg.l2promo)
+            org = home.xoff * home.elem
+            params = temporal.pack_params(tm, src_buf.ptr + org, bbuf.ptr + org, dst_buf.ptr + org,
+                                          home, s_lo, s_hi, geo, write_b=last or not temporal.SKIP_MID_B, cz=cz)
+            self._launch(kern, (geo["blocks"], 1, 1), params, tag=("tb", K))
 
     # -- node -> kernel launch ----------------------------------------------
     def _tmap(self, buf, box, l2promo: int = 3) -> bytes:

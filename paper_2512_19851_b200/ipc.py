@@ -13,8 +13,15 @@ The data path never touches the host:
 * halo strips are pulled by the receiver's copy kernel straight out of the
   owner's mapped buffer (NVLink P2P between GPUs; also works between processes
   sharing one GPU, which is how the 1-GPU test box exercises this path);
-* the per-round sequence counters live in a shared-memory page (/dev/shm), so
-  the host-side handshake is a few loads/stores, not a socket round trip.
+* round signalling is DEVICE-side: every rank owns two 32-bit flag words
+  (READY, PULLED) in its exported arena; a round's READY is a stream write
+  (`est_flag_write`, release) behind the array's last writer, the receiver's
+  copy stream waits on the owner's flag word (`est_flag_wait`, a front-end
+  semaphore acquire over NVLink) before its pull, and PULLED gates the owner's
+  next overwrite. The host never waits on a peer inside a batch: no per-round
+  host handshake, no IPC event waits (24 us each on the host, profiles/
+  r2_ipc_host_profile.txt). A /dev/shm page keeps only the abort flags, which
+  `sync` polls so a dead peer raises instead of hanging the stream.
 """
 
 from __future__ import annotations
@@ -30,6 +37,8 @@ from .device import Device, PinnedBuffer
 from .exchange import GpuExchangeManager
 from .executor import GpuExecutor
 from .tiles import ArrayInfo, GpuTileStore, TileBuffer, decompose
+from .codegen import ELEM
+from .device import COMPUTE, COPY
 from .transport import RING, LocalPeerTransport, TransportAborted
 from .wire import DTYPE_F64
 
@@ -58,17 +67,38 @@ class SharedCounters:
             pass
 
 
+READY_OFF, PULLED_OFF = 0, 128  # byte offsets of the two flag words (separate 128-B lines)
+FLAGS_KEY = (("flags",), -1)     # buffer-table key of a rank's flag block
+
+
 class IpcPeerTransport(LocalPeerTransport):
-    """transport.py protocol over CUDA IPC handles + shared-memory counters."""
+    """transport.py round protocol across processes: CUDA IPC buffers and
+    device-side flag words (see the module docstring).
+
+    Per round r (sequence shared by all ranks, value r + 1 on the wire):
+      post      READY := r+1 on the compute stream (behind the array's writer)
+      finish    per remote owner p: lane waits READY[p] >= r+1, pulls the
+                strips, then PULLED := r+1 on the lane
+      before_write  (the next overwrite of the array) compute waits
+                PULLED[p] >= r+1 for every peer that read from us in round r
+    Monotonic values make a later round's write only over-synchronise. PULLED
+    is written from the copy lane for overlapped rounds and from the compute
+    stream otherwise; the executor joins the copy lane into the compute
+    stream (`join_copy`) before any later compute-stream write, so the word
+    never goes backwards."""
 
     def __init__(self, job: "IpcGpuJob"):
+        from .pool import device_alloc
+
         self.job = job
         self.w = job.rank
         self.store = job.store
         self.dev = job.dev
         self.seq = 0
-        self.ready = [self.dev.event(interprocess=True) for _ in range(RING)]
-        self.pulled = [self.dev.event(interprocess=True) for _ in range(RING)]
+        self.flags = device_alloc(self.dev, 256)  # [READY_OFF] ready, [PULLED_OFF] pulled; zeroed
+        self.ready = [self.dev.event() for _ in range(RING)]   # intra-process: copy lane after compute
+        self.pulled = [self.dev.event() for _ in range(RING)]  # intra-process: compute after copy lane
+        self.peer_flag_base: dict = {}
         self.readers: dict = {}
         self.pull_launches = 0
         self.peer_events: dict = {}
@@ -82,13 +112,10 @@ class IpcPeerTransport(LocalPeerTransport):
 
     # -- handle exchange ---------------------------------------------------------
     def event_handles(self) -> dict:
-        return {"ready": [e.ipc_handle() for e in self.ready],
-                "pulled": [e.ipc_handle() for e in self.pulled]}
+        return {}  # rounds are signalled through device flags (no IPC events)
 
     def open_peer_events(self, table: dict) -> None:
-        """Remember the peers' event handles; each is opened on first use
-        (only halo neighbours ever wait on each other's events)."""
-        self.peer_event_handles = {o: h for o, h in table.items() if o != self.w}
+        self.peer_event_handles = {}
 
     def buffer_table(self) -> dict:
         """(coords, array) -> (arena serial, arena IPC handle, offset, extents,
@@ -101,6 +128,12 @@ class IpcPeerTransport(LocalPeerTransport):
                 serial, handle, off = pool.locate(buf.ptr)
                 out[(tuple(coords), array)] = (serial, handle, off, buf.ext[3 - buf.rank:],
                                                buf.depth[3 - buf.rank:], buf.dtype, buf.serial)
+        for (coords, array), buf in self.store.twins.items():
+            serial, handle, off = pool.locate(buf.ptr)
+            out[(tuple(coords), ("twin", array))] = (serial, handle, off, buf.ext[3 - buf.rank:],
+                                                      buf.depth[3 - buf.rank:], buf.dtype, buf.serial)
+        serial, handle, off = pool.locate(self.flags)
+        out[FLAGS_KEY] = (serial, handle, off, (), (), 0, 0)
         return out
 
     def open_peer_buffers(self, tables: list) -> None:
@@ -137,14 +170,13 @@ class IpcPeerTransport(LocalPeerTransport):
                     nb = neighbour(self.store.decomp, info.rank, coords, d)
                     if nb is None or owners.get(nb, self.w) == self.w:
                         continue
-                    key = (owners[nb], tuple(nb), a)
-                    if key in self.peer_tables:
-                        self.peer_buffer(*key)
-                        peers.add(owners[nb])
+                    for arr in (a, ("twin", a)):
+                        key = (owners[nb], tuple(nb), arr)
+                        if key in self.peer_tables:
+                            self.peer_buffer(*key)
+                            peers.add(owners[nb])
         for p in peers:
-            for kind in ("ready", "pulled"):
-                for slot in range(len(self.peer_event_handles.get(p, {}).get(kind, []))):
-                    self.peer_event(p, kind, slot)
+            self.peer_flags(p)
         return len(self.peer_maps) - before
 
     def close_peer_buffers(self) -> None:
@@ -185,26 +217,62 @@ class IpcPeerTransport(LocalPeerTransport):
             ev = lst[slot] = self.dev.open_event(self.peer_event_handles[owner][kind][slot])
         return ev
 
-    def wait_seq(self, owner: int, kind: str, r: int) -> None:
-        row = 0 if kind == "ready" else 1
-        arr = self.job.counters.arr
-        t0 = time.perf_counter()
-        spins = 0
-        while arr[row, owner] < r:
-            if arr[2].any():
-                raise TransportAborted(f"peer aborted while waiting for {kind}[{owner}] >= {r}")
-            spins += 1
-            if spins > 2000:
-                time.sleep(2e-5)
-            if time.perf_counter() - t0 > self.job.timeout_s:
-                raise TransportAborted(f"timeout waiting for {kind}[{owner}] >= {r}")
-        self.spin_s += time.perf_counter() - t0
+    def peer_flags(self, owner: int) -> int:
+        """Device address of `owner`'s flag block (its arena, mapped once)."""
+        base = self.peer_flag_base.get(owner)
+        if base is None:
+            aserial, handle, off = self.peer_tables[(owner,) + FLAGS_KEY][:3]
+            arena = self.arena_maps.get((owner, aserial))
+            if arena is None:
+                arena = self.arena_maps[(owner, aserial)] = self.dev.ipc_open(handle)
+            base = self.peer_flag_base[owner] = arena + off
+        return base
 
-    def publish(self, kind: str, r: int) -> None:
-        self.job.counters.arr[0 if kind == "ready" else 1, self.w] = r
+    # -- the round protocol on device flags ---------------------------------------
+    chains_ok = True  # peers map each other's twin buffers (buffer_table), so slabs chain
+
+    def post(self, array: int, epoch: int, remote, local_boxes, twin: bool = False):
+        r = self.seq
+        self.seq += 1
+        elem = ELEM[self.store.arrays[array].dtype]
+        self.dev.flag_write(self.flags + READY_OFF, r + 1, COMPUTE)
+        if local_boxes:
+            self.dev.copy_boxes(local_boxes, elem)
+        return (array, r, remote, elem, twin)
+
+    def finish(self, token, overlap: bool = False) -> None:
+        array, r, remote, elem, twin = token
+        slot = r % RING
+        lane = COMPUTE
+        if overlap and remote:
+            lane = COPY
+            self.ready[slot].record(COMPUTE)  # previous readers of the ghost are done
+            self.ready[slot].wait(COPY)
+        peers = sorted({owner for _, _, _, owner in remote})
+        for p in peers:
+            self.dev.flag_wait(self.peer_flags(p) + READY_OFF, r + 1, lane)
+        if remote:
+            self.dev.copy_boxes(self._pull_boxes(array, remote, twin), elem, lane)
+            self.pull_launches += 1
+        self.dev.flag_write(self.flags + PULLED_OFF, r + 1, lane)
+        if lane != COMPUTE:
+            self.pulled[slot].record(lane)
+        if peers:
+            self.readers[array] = (r, peers)
+
+    def join_copy(self, r: int) -> None:
+        self.pulled[r % RING].wait(COMPUTE)
+
+    def before_write(self, array: int) -> None:
+        ent = self.readers.pop(array, None)
+        if ent is None:
+            return
+        r, peers = ent
+        for p in peers:
+            self.dev.flag_wait(self.peer_flags(p) + PULLED_OFF, r + 1, COMPUTE)
 
     def before_realloc(self) -> None:
-        self.dev.sync()
+        self.job.sync()
         self.job.barrier()
         self.readers.clear()
         self.close_peer_buffers()
@@ -217,12 +285,8 @@ class IpcPeerTransport(LocalPeerTransport):
 
     def close(self) -> None:
         self.close_peer_buffers()
+        self.peer_flag_base.clear()
         self.close_arenas()
-        for evs in self.peer_events.values():
-            for lst in evs.values():
-                for e in lst:
-                    if e is not None:
-                        e.close()
         for e in self.ready + self.pulled:
             e.close()
 
@@ -295,7 +359,7 @@ class IpcGpuJob:
         return self.group.allgather(obj)
 
     def exchange_buffers(self) -> None:
-        self.dev.sync()
+        self.sync()
         tables = self._all_gather(self.transport.buffer_table())
         self.transport.open_peer_buffers(tables)
         self.transport.map_neighbours()
@@ -354,10 +418,32 @@ class IpcGpuJob:
             raise
 
     def sync(self) -> None:
+        """Drain both streams. They may be parked on a peer's flag word, so
+        this polls (instead of blocking in the driver) and raises
+        TransportAborted if a peer flagged an abort or the wait outlives
+        `timeout_s` - a dead peer must not hang the worker."""
+        from .device import COMPUTE, COPY
+
+        evs = [self.dev.event(), self.dev.event()]
+        evs[0].record(COMPUTE)
+        evs[1].record(COPY)
+        t0 = time.perf_counter()
+        nap = 2e-5
+        try:
+            while not all(e.done() for e in evs):
+                if self.counters is not None and self.counters.arr[2].any():
+                    raise TransportAborted("a peer aborted while this worker's streams were waiting on it")
+                if time.perf_counter() - t0 > self.timeout_s:
+                    raise TransportAborted(f"device work did not drain within {self.timeout_s:.0f} s")
+                time.sleep(nap)
+                nap = min(nap * 2, 1e-3)
+        finally:
+            for e in evs:
+                e.close()
         self.dev.sync()
 
     def fetch_local(self, array: int, bounds=None) -> list:
-        self.dev.sync()
+        self.sync()
         shape = self.shapes[array]
         bounds = tuple(bounds) if bounds is not None else tuple((0, e) for e in shape)
         nbytes = int(np.prod([b - a for a, b in bounds])) * 8
@@ -382,7 +468,7 @@ class IpcGpuJob:
 
     def hash_local(self, array: int) -> int:
         """This rank's partial of the whole-array content hash (its tiles)."""
-        self.dev.sync()
+        self.sync()
         return self.store.hash(array) if self.store is not None and self.store.tiles else 0
 
     def hash(self, array: int) -> int:

@@ -274,7 +274,7 @@ class _Emitter:
         a("struct __align__(64) Tmap { unsigned long long w[16]; };")
         a("struct __align__(64) Params { Tmap tm;")
         a("  unsigned long long src, bhome, adst;  // padded-box origins: A now, B (in place), A next")
-        a("  int npz, npy, npx, sz0, sz1, sy0, sy1, sx0, sx1, xt0, nbx, nby, zc, nzc, wb; };")
+        a("  int npz, npy, npx, sz0, sz1, sy0, sy1, sx0, sx1, xt0, nbx, nby, zc, nzc, wb, cz0, cz1; };")
         a(_PTX_HELPERS)
         a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
         a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
@@ -331,7 +331,7 @@ class _Emitter:
         a(f"  const bool act = tid < {lay['nact']};")
         a(f"  const bool xw = (lane & {8 if V == 2 else 16}) != 0;  // crossed west/east neighbour loads")
         a(f"  const int sw = xw ? {V + 1} : 0;")
-        a("  const int wb = p.wb, sz0 = p.sz0, sz1 = p.sz1, npz = p.npz;")
+        a("  const int wb = p.wb, cz0 = p.cz0, cz1 = p.cz1, npz = p.npz;  // cz: S's planes in reach")
         a(f"  const int cc = tid % {P1}, gg = tid / {P1};  // vector column / row group in the step-1 frame")
         a(f"  const int off0 = ({e[0] - e[1]} + gg * {RPT}) * {W0} + {m[0] - m[1]} + cc * {V};  // input frame")
         a(f"  const int off1 = gg * {RPT} * {W1} + cc * {V};  // step-1 frame (rings)")
@@ -394,7 +394,7 @@ class _Emitter:
             a(f"{i3}const int t = t0 + {mm};")
             for j in range(1, K):
                 a(f"{i3}const int u{j} = zs - {(K + j) * rz} + t;  // step-{j} plane")
-                a(f"{i3}const bool zs{j} = u{j} >= sz0 && u{j} < sz1, zp{j} = u{j} >= 0 && u{j} < npz;")
+                a(f"{i3}const bool zs{j} = u{j} >= cz0 && u{j} < cz1, zp{j} = u{j} >= 0 && u{j} < npz;")
                 if edge:
                     # stored values outside S, prefetched before the plane's wait
                     home = "bmem" if j % 2 == 1 else "asrc"
@@ -549,17 +549,24 @@ def item_geometry(s_lo, s_hi, sm_count: int, lay: dict, xoff: int = 0) -> dict:
 
 
 def pack_params(tmap: bytes, src: int, bhome: int, adst: int, buf, s_lo, s_hi, geo: dict,
-                write_b: bool = True) -> bytes:
+                write_b: bool = True, cz=None) -> bytes:
     """Params block (layout mirrored in `source`). Pointers are padded-box
     origins (buffer base + xoff elements). `write_b` False skips B's stores:
     inside a run only the last chain's B survives (the next chain overwrites
-    B before anything reads it), so earlier chains move 16 B per K LUP."""
+    B before anything reads it), so earlier chains move 16 B per K LUP.
+    `cz` = the padded planes [cz0, cz1) where the intermediate steps COMPUTE
+    the statement (the global output slice within reach of this tile): on a
+    slab of a multi-tile job it extends past the tile's own output planes
+    into the ghost planes that belong to the neighbour's output (default:
+    the tile's own output planes [s_lo[0], s_hi[0]))."""
     assert len(tmap) == 128
     npz, npy, npx = buf.nz, buf.pz // buf.py, buf.ext[2] + 2 * buf.depth[2]
+    cz0, cz1 = cz if cz is not None else (s_lo[0], s_hi[0])
     out = bytearray(tmap)
     out += struct.pack("<QQQ", src, bhome, adst)
-    out += struct.pack("<15i", npz, npy, npx, s_lo[0], s_hi[0], s_lo[1], s_hi[1],
-                       s_lo[2], s_hi[2], geo["xt0"], geo["nbx"], geo["nby"], geo["zc"], geo["nzc"], int(write_b))
+    out += struct.pack("<17i", npz, npy, npx, s_lo[0], s_hi[0], s_lo[1], s_hi[1],
+                       s_lo[2], s_hi[2], geo["xt0"], geo["nbx"], geo["nby"], geo["zc"], geo["nzc"], int(write_b),
+                       cz0, cz1)
     return bytes(out) + b"\0" * ((-len(out)) % 64)
 
 

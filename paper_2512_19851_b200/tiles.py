@@ -202,6 +202,9 @@ class GpuTileStore:
         self.version = 0  # bumped whenever any buffer is (re)allocated or dropped
         self._epochs: dict = {}  # array -> local epoch (also valid with no tiles)
         self._ghosts: dict = {}
+        self.phys_depth: dict = {}  # array -> allocated ghost frame (>= logical; also with no tiles)
+        self.twins: dict = {}       # (coords, array) -> twin TileBuffer of a temporal chain's input
+        self.twin_sig: dict = {}    # array -> (info, frame, store version) the twins were made for
 
     # -- creation / capacity ------------------------------------------------
     def create_array(self, info: ArrayInfo) -> None:
@@ -228,25 +231,46 @@ class GpuTileStore:
             if d >= e:
                 raise OffsetExceedsTileWidth(f"ghost depth {d} >= tile width {e} for array {array}")
 
-    def ensure_ghost_capacity(self, array: int, depth) -> bool:
-        """Grow (never shrink) the ghost frame on the device; True if any grew."""
+    def ensure_ghost_capacity(self, array: int, depth, phys=None) -> bool:
+        """Grow (never shrink) the ghost frame on the device; True if the
+        LOGICAL depth (the reference's, grid.py:164-184) grew on any tile.
+
+        `phys` (>= depth) is the frame actually allocated: rank-3 slabs of a
+        multi-tile job keep K*rz planes of ghost so a K-sweep temporal chain
+        can run on one halo round (executor.temporal_schedule). A purely
+        physical growth keeps the ghost contents (the whole old padded box is
+        copied), so no epoch changes; a logical growth copies the interior and
+        the caller bumps the local epoch as the reference does."""
         self.check_depth_fits(array, depth)
-        grew = False
+        rank = self.arrays[array].rank
+        phys = tuple(max(a, b) for a, b in zip(depth, phys if phys is not None else depth))
+        self.phys_depth[array] = tuple(max(a, b) for a, b in zip(self.phys_depth.get(array, phys), phys))
+        grew = grew_buf = False
         for tile in self.tiles.values():
             old = tile.depths[array]
             new = tuple(max(a, b) for a, b in zip(old, depth))
-            if new == old:
-                continue
             src = tile.buffers[array]
-            dst = TileBuffer(self.dev, src.ext[3 - src.rank:], new, src.dtype)
+            have = src.depth[3 - rank:]
+            want = tuple(max(a, b) for a, b in zip(have, phys))
+            if new == old and want == tuple(have):
+                continue
             ext = src.ext[3 - src.rank:]
-            self.dev.copy_box(src.box_to(dst.interior_addr((0,) * src.rank), dst.py, dst.pz,
-                                         (0,) * src.rank, ext), src.elem, COMPUTE)
+            dst = TileBuffer(self.dev, ext, want, src.dtype)
+            if new == old:
+                # physical only: carry the valid ghost frame along
+                lo = tuple(h - o for h, o in zip(want, have))
+                whole = tuple(e + 2 * o for e, o in zip(ext, have))
+                self.dev.copy_box(src.box_to(dst.addr(*pad3(lo, 0)), dst.py, dst.pz,
+                                             (0,) * src.rank, whole, padded=True), src.elem, COMPUTE)
+            else:
+                self.dev.copy_box(src.box_to(dst.interior_addr((0,) * src.rank), dst.py, dst.pz,
+                                             (0,) * src.rank, ext), src.elem, COMPUTE)
+                grew = True
             src.free()  # est_free synchronises the lanes before releasing
             tile.buffers[array] = dst
             tile.depths[array] = new
-            grew = True
-        if grew:
+            grew_buf = True
+        if grew_buf:
             self.version += 1
         return grew
 
@@ -424,6 +448,9 @@ class GpuTileStore:
             for buf in tile.buffers.values():
                 buf.free()
             tile.buffers.clear()
+        for buf in self.twins.values():
+            buf.free()
+        self.twins.clear()
 
 
 # --------------------------------------------------------------------------

@@ -23,8 +23,9 @@ it was published, so no cycle can form.
 
 `LocalPeerTransport` runs this between workers of one process (threads; the
 reference LocalMesh analogue, usable on a single GPU). `ipc.IpcPeerTransport`
-runs the same protocol across processes with CUDA IPC memory/event handles and
-shared-memory sequence counters.
+runs the same round protocol across processes entirely on the device: CUDA IPC
+buffers plus READY / PULLED flag words written and waited on by the streams
+themselves (stream memory operations), so no host thread waits on a peer.
 """
 
 from __future__ import annotations
@@ -122,10 +123,12 @@ class LocalPeerTransport:
         self.group.publish(table, self.w, r)
 
     # -- protocol -------------------------------------------------------------
-    def exchange(self, array: int, epoch: int, remote, local_boxes) -> None:
-        self.finish(self.post(array, epoch, remote, local_boxes), overlap=False)
+    chains_ok = False  # the in-process peers do not share the temporal chains' twin buffers
 
-    def post(self, array: int, epoch: int, remote, local_boxes):
+    def exchange(self, array: int, epoch: int, remote, local_boxes, twin: bool = False) -> None:
+        self.finish(self.post(array, epoch, remote, local_boxes, twin), overlap=False)
+
+    def post(self, array: int, epoch: int, remote, local_boxes, twin: bool = False):
         """Steps 1-2: READY record + co-located copies; the peer pull is left
         to `finish`, which the executor may defer past the next node's
         interior launch (halo/compute overlap)."""
@@ -137,14 +140,14 @@ class LocalPeerTransport:
         self.publish("ready", r)
         if local_boxes:
             self.dev.copy_boxes(local_boxes, elem)
-        return (array, r, remote, elem)
+        return (array, r, remote, elem, twin)
 
     def finish(self, token, overlap: bool = False) -> None:
         """Steps 3-4. With `overlap` the pull runs on the COPY stream (after
         this worker's own READY, so the previous readers of the ghost are
         done) and the compute stream only joins it before the boundary work
         (`join_copy`)."""
-        array, r, remote, elem = token
+        array, r, remote, elem, twin = token
         slot = r % RING
         lane = COMPUTE
         if overlap and remote:
@@ -155,23 +158,28 @@ class LocalPeerTransport:
             self.wait_seq(p, "ready", r)
             self.peer_event(p, "ready", slot).wait(lane)
         if remote:
-            ck = (array, self.store.version, self.peer_version, id(remote))
-            boxes = self._pulls.get(ck)
-            if boxes is None:
-                boxes = []
-                for coords, d, nb, owner in remote:
-                    src_buf, src_addr = self.peer_buffer(owner, nb, array)
-                    dst_buf = self.store.tiles[coords].buffers[array]
-                    boxes.append(strip_copy(src_buf, dst_buf, d, src_addr_override=src_addr))
-                if len(self._pulls) > 1024:
-                    self._pulls.clear()
-                self._pulls[ck] = boxes
-            self.dev.copy_boxes(boxes, elem, lane)
+            self.dev.copy_boxes(self._pull_boxes(array, remote, twin), elem, lane)
             self.pull_launches += 1
         self.pulled[slot].record(lane)
         self.publish("pulled", r)
         if peers:
             self.readers[array] = (r, peers)
+
+    def _pull_boxes(self, array: int, remote, twin: bool = False) -> list:
+        """Copy descriptors of one round's remote strips (cached per layout);
+        `twin`: between the temporal chains' twin buffers (mid-run)."""
+        ck = (array, self.store.version, self.peer_version, id(remote), twin)
+        boxes = self._pulls.get(ck)
+        if boxes is None:
+            boxes = []
+            for coords, d, nb, owner in remote:
+                src_buf, src_addr = self.peer_buffer(owner, nb, ("twin", array) if twin else array)
+                dst_buf = self.store.twins[(coords, array)] if twin else self.store.tiles[coords].buffers[array]
+                boxes.append(strip_copy(src_buf, dst_buf, d, src_addr_override=src_addr))
+            if len(self._pulls) > 1024:
+                self._pulls.clear()
+            self._pulls[ck] = boxes
+        return boxes
 
     def join_copy(self, r: int) -> None:
         """Compute stream waits for the overlapped pull of round r."""

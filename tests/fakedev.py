@@ -85,6 +85,12 @@ class FakeDevice:
     def stream_sync(self, s):
         pass
 
+    def flag_write(self, addr, value, stream=0):
+        self.log.append(("flag_write", addr, value, stream))
+
+    def flag_wait(self, addr, value, stream=0):
+        self.log.append(("flag_wait", addr, value, stream))
+
     def event(self, interprocess=False):
         return FakeEvent(self, f"{self.tag}-ev{next(self._ids)}")
 

@@ -34,10 +34,16 @@ def _split(dag, size):
     return out
 
 
-def host_logic_rank(rank, world, kind, odf, batch):
-    """CPU: fake device, real executor / exchange / IPC transport host logic."""
+def host_logic_rank(rank, world, kind, odf, batch, chains=False):
+    """CPU: fake device, real executor / exchange / IPC transport host logic.
+    `chains`: temporal chains at test sizes (slab chains across processes)."""
     import paper_2512_19851_b200.ipc as ipc
     from fakedev import FakeDevice
+
+    if chains:
+        from paper_2512_19851_b200 import temporal
+
+        temporal.MIN_POINTS = 0
 
     ipc.Device = lambda device=0: FakeDevice(device, tag=f"r{rank}")
     prog, _ = _program(kind)
@@ -53,16 +59,25 @@ def host_logic_rank(rank, world, kind, odf, batch):
            "launches": sum(s.kernel_launches for s in stats),
            "strips": len(strips), "seq": job.transport.seq,
            "copy_lane_pulls": job.dev.lane_copies.get(1, 0),
-           "tiles": sorted(job.store.tiles)}
+           "tiles": sorted(job.store.tiles),
+           "tb_launches": sum(1 for e in job.dev.log if e[0] == "launch" and e[2] == "est_tb"),
+           "twins": len(job.store.twins),
+           "peer_twins": sum(1 for k in job.transport.peer_maps if isinstance(k[2], tuple)),
+           "flag_waits": sum(1 for e in job.dev.log if e[0] == "flag_wait")}
     job.close()
     return out
 
 
-def gpu_rank(rank, world, kind, odf, batch):
-    """GPU: real IPC job; several processes may share cuda:0."""
+def gpu_rank(rank, world, kind, odf, batch, chains=False):
+    """GPU: real IPC job; several processes may share cuda:0. `chains`:
+    temporal chains at test sizes (slab chains across processes)."""
     from oracle.oracle import bits_equal, reference_execute_dag
     from paper_2512_19851_b200.ipc import IpcGpuJob
 
+    if chains:
+        from paper_2512_19851_b200 import temporal
+
+        temporal.MIN_POINTS = 0
     prog, names = _program(kind)
     job = IpcGpuJob(rank, world, device=0, odf=odf)
     for aid in sorted(prog.shapes):
@@ -72,8 +87,9 @@ def gpu_rank(rank, world, kind, odf, batch):
     want = reference_execute_dag(prog.dag, prog.shapes)
     ok = {aid: bits_equal(job.fetch(aid), want[aid]) for aid in prog.shapes}
     rounds = job.rounds_by_array()
+    twins = len(job.store.twins)
     job.close()
-    return {"ok": ok, "rounds": rounds}
+    return {"ok": ok, "rounds": rounds, "twins": twins}
 
 
 def migrate_rank(rank, world, kind, shrink_to):

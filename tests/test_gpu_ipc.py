@@ -1,6 +1,7 @@
 """Multi-PROCESS GPU workers (CUDA IPC transport) on one GPU: each rank is a
 separate process with its own CUDA context; halos are pulled out of the peer
-process's HBM buffers through IPC handles, ordered by IPC events."""
+process's HBM buffers through IPC handles, ordered by device-side flag words
+(stream write / wait on 32-bit values in the peers' exported arenas)."""
 
 import pytest
 
@@ -20,3 +21,16 @@ def test_ipc_workers_bit_exact(kind, world, odf, batch):
     for r in res:
         assert all(r["ok"].values()), r["ok"]
         assert r["rounds"] == want
+
+
+@pytest.mark.parametrize("world,odf,batch", [(2, 1, 8), (2, 2, 20), (4, 1, 12)])
+def test_ipc_slab_chains_bit_exact(world, odf, batch):
+    """Temporal chains on the z-slabs of a multi-process job: each rank's
+    chain reads A's 2-plane halo pulled out of its neighbours' buffers (home
+    or twin, alternating per chain), bit-exact with the reference round counts."""
+    res = spawn_local_job(world, gpu_rank, "heat3d", odf, batch, True, timeout=600)
+    want = expected_rounds("heat3d", batch)
+    for r in res:
+        assert all(r["ok"].values()), r["ok"]
+        assert r["rounds"] == want
+        assert r["twins"] == odf, "the slab chains did not run"

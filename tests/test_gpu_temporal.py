@@ -310,3 +310,34 @@ def test_random_z_star_chains(seed, mode):
             assert bits_equal(job.fetch(aid), want[aid]), (seed, aid)
     finally:
         job.close()
+
+
+@pytest.mark.parametrize("n,iters,odf,batch", [(32, 8, 2, None), (48, 12, 4, None), (40, 9, 2, 7),
+                                               (64, 16, 4, 10)])
+def test_slab_chains_bit_exact(n, iters, odf, batch, mode):
+    """Several z-slabs in one process: every slab runs the chain on its own
+    K*rz-deep halo of A; the intermediate array's ghost planes are computed
+    in-chain (virtual rounds). Bit-identical to the oracle, with the
+    reference's round counts."""
+    from oracle.oracle import EpochSimulator
+    from paper_2512_19851_b200.analysis import analyze_dag
+    from paper_2512_19851_b200.ir import Dag, DagNode, compute_edges
+
+    prog = DagProgram()
+    heat3d_program(prog, n, iters, seed_fills=10)
+    want = strict_execute_dag(prog.dag, prog.shapes)
+    job, stats = run_program(prog, workers=1, odf=odf, batch=batch)
+    try:
+        if batch is None and mode == "k2":  # multi-tile chains are K = 2 only (executor._slab_chains_ok)
+            assert job.executors[0].store.twins, "slab chains did not run"
+        for aid in prog.shapes:
+            assert bits_equal(job.fetch(aid), want[aid]), (n, iters, odf, aid)
+        sim = EpochSimulator()
+        nodes = prog.dag.nodes
+        for k in range(0, len(nodes), batch or len(nodes)):
+            part = [DagNode(i, x.statements) for i, x in enumerate(nodes[k:k + (batch or len(nodes))])]
+            d = Dag(part, compute_edges(part), prog.dag.ast_table)
+            sim.simulate_batch(d, analyze_dag(d, prog.shapes))
+        assert job.rounds_by_array() == sim.rounds
+    finally:
+        job.close()

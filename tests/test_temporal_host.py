@@ -89,8 +89,9 @@ def test_twin_buffer_and_complement_copy():
     dev.copies.clear()
     ex.execute_batch(step.dag)
     a = step.dag.nodes[0].statements[0].inputs[0]
-    twin = ex._scratch[a]
-    home = next(iter(store.tiles.values())).buffers[a]
+    coords = next(iter(store.tiles))
+    twin = store.twins[(coords, a)]
+    home = store.tiles[coords].buffers[a]
     assert (twin.py, twin.pz, twin.xoff, twin.nbytes) == (home.py, home.pz, home.xoff, home.nbytes)
     strips = [c for c in dev.copies if c[0] == "strip"]
     # padded box 18^3 minus S = [1,17)^3 in padded coords ([2,16) after depth 1) -> 6 boxes
@@ -102,12 +103,64 @@ def test_twin_buffer_and_complement_copy():
     assert twin.ptr == 0
 
 
-def test_no_chains_with_several_tiles_or_workers():
+def test_slab_chains_keep_reference_bookkeeping():
+    """Several z-slabs in one process (odf 2 / 4): chains run per slab on a
+    2-deep halo of A (physical ghost frame K*rz, logical depth 1 as in the
+    reference), the intermediate array's rounds are virtual, and epochs,
+    ghost generations, rounds, net messages and launch counts equal the
+    unfused execution batch for batch."""
+    K = temporal.DEFAULT.k
+    for odf in (2, 4):
+        setup, step = _heat(8, n=16)
+        res = []
+        for on in (True, False):
+            ex, store, mgr, dev = _executor(setup.shapes, 1, odf, temporal_on=on)
+            ex.execute_batch(setup.dag)
+            st = [ex.execute_batch(step.dag, b"k") for _ in range(3)]
+            if on:
+                assert _names(dev).count("est_tb") == 3 * odf * 8 // K  # every slab, every chain
+                assert all(store.phys_depth[a] == (K, 1, 1) for a in store.arrays)
+                assert all(t.depths[a] == (1, 1, 1) for t in store.tiles.values() for a in store.arrays)
+                assert all(b.depth == (K, 1, 1) for t in store.tiles.values() for b in t.buffers.values())
+                assert len(store.twins) == odf  # one twin per slab for the chains' input array
+            res.append(({a: (store.local_epoch(a), store.ghost_epoch(a)) for a in store.arrays},
+                        dict(mgr.rounds_started),
+                        [(s.nodes_executed, s.kernel_launches, s.rounds, s.net_messages) for s in st]))
+        assert res[0] == res[1], odf
+
+
+def test_slab_chain_rounds_alternate_home_and_twin():
+    """Mid-run, A lives in the twins: the halo round before an odd chain moves
+    strips between twins (2 planes = the physical frame), before an even one
+    between the home buffers."""
     setup, step = _heat(8, n=16)
-    for workers, odf in ((1, 2), (2, 1)):
-        ex, store, mgr, dev = _executor(setup.shapes, workers, odf)
-        plans = [compile_plan(n, step.dag.ast_table) for n in step.dag.nodes]
-        assert ex.temporal_schedule(step.dag, plans) == {}
+    ex, store, mgr, dev = _executor(setup.shapes, 1, 2)
+    ex.execute_batch(setup.dag)
+    ex.execute_batch(step.dag)
+    dev.copies.clear()
+    ex.execute_batch(step.dag)
+    a = step.dag.nodes[0].statements[0].inputs[0]
+    homes = {t.buffers[a].ptr: t.buffers[a] for t in store.tiles.values()}
+    twins = {store.twins[(c, a)].ptr: store.twins[(c, a)] for c in store.tiles}
+
+    def owner(addr, table):
+        return any(p <= addr < p + b.nbytes for p, b in table.items())
+
+    strips = [c for c in dev.copies if c[0] == "strip" and c[3:] == (16, 16, temporal.DEFAULT.k)]  # halo planes
+    in_twin = [owner(c[2], twins) for c in strips]
+    assert in_twin and any(in_twin) and not all(in_twin)
+    assert all(owner(c[1], twins) == t for c, t in zip(strips, in_twin))
+    assert all(owner(c[2], homes) != t for c, t in zip(strips, in_twin))
+
+
+def test_no_chains_between_in_process_peer_workers():
+    from paper_2512_19851_b200.transport import LocalPeerGroup, LocalPeerTransport
+
+    setup, step = _heat(8, n=16)
+    ex, store, mgr, dev = _executor(setup.shapes, 2, 1)
+    ex.transport = LocalPeerTransport(LocalPeerGroup([store, store]), 0)
+    plans = [compile_plan(n, step.dag.ast_table) for n in step.dag.nodes]
+    assert ex.temporal_schedule(step.dag, plans, phys={0: (2, 1, 1), 1: (2, 1, 1)}) == {}
 
 
 def test_chain_requires_same_statement_and_ping_pong():
