@@ -67,17 +67,23 @@ def _run(suite: str, select: str):
     return subprocess.run(cmd, cwd=SUITES, env=env, capture_output=True, text=True, timeout=1800)
 
 
+def _failing_lines(stdout: str) -> list:
+    """The source lines pytest marks as the failing statement ('>' prefix)."""
+    return [ln for ln in stdout.splitlines() if re.match(r"^>\s+\S", ln)]
+
+
 def test_criterion_6_transparency_on_gpu_workers():
     out = _run("test_acceptance.py", "criterion_6")
     tail = out.stdout[-4000:] + out.stderr[-2000:]
     if out.returncode == 0:
         return
     # the trend half prints the payload series only after the rescaled run
-    # matched the oracle (test_acceptance.py:292-307); the failure must be the
-    # trend assertion itself
-    assert "rescaled run diverged" not in out.stdout, tail
+    # matched the oracle (test_acceptance.py:292-307); the failing line (pytest
+    # marks it with '>' in the traceback, which also echoes the test's source,
+    # so bare substrings of the source prove nothing) must be a trend assertion
     assert "payload MB [16, 64, 256]" in out.stdout, tail
-    assert re.search(r"not monotone|r >= 0\.9|assert r >=", out.stdout), tail
+    failing = _failing_lines(out.stdout)
+    assert failing and all(re.search(r"costs_ms|\br >= 0\.9", ln) for ln in failing), tail
 
 
 def test_criterion_5_pipelining_on_gpu_workers():
@@ -88,7 +94,8 @@ def test_criterion_5_pipelining_on_gpu_workers():
     # "walls by threshold" is printed after the equality and batch-count
     # assertions (test_acceptance.py:255-261); only the timing line may fail
     assert "walls by threshold:" in out.stdout, tail
-    assert re.search(r"assert walls\[100\] <= walls\[1\]", out.stdout), tail
+    failing = _failing_lines(out.stdout)
+    assert failing and all("walls[100] <= walls[1]" in ln for ln in failing), tail
 
 
 @pytest.mark.parametrize("suite", ["test_daemon.py", "test_runtime.py", "test_acceptance.py"])
