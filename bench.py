@@ -61,6 +61,9 @@ WORKLOADS = {
                label="C3: 2-D acoustic wave r=2 16384^2 fp32 (BASELINE configs[2])"),
     "c1": dict(kind="laplace", n=1024, iters_per_step=100, dtype="f64", steps=2000,  # >= 0.5 s timed (clock samples)
                label="C1: 2-D 5-point Jacobi 1024^2 fp64 (BASELINE configs[0])"),
+    # not a BASELINE config: the paper's 2-D Laplace weak-scaling per-GPU size
+    "lap16k": dict(kind="laplace", n=16384, iters_per_step=100, dtype="f64",
+                   label="paper shape: 2-D 5-point Jacobi 16384^2 fp64 per GPU"),
 }
 METRIC = "GLUP/s (grid-point updates/s)"
 L2_BYTES = 126 << 20        # B200 L2
@@ -99,6 +102,18 @@ def bytes_per_launch(w, tag) -> int:
     kind, sweeps = tag
     if kind in ("res", "rsm"):  # resident chains: every sweep counts as a full pass (data in L2 / smem)
         return bytes_per_iter(w) * sweeps
+    if kind == "tc":
+        # rank-2 two-sweep chain (temporal2d.py). Wave rotation: u1 read once
+        # (with its halo), u0 read once, u2 and the new u0 written once;
+        # ping-pong: A read and written once, B once per run
+        from paper_2512_19851_b200 import temporal
+        m = w["n"] - (4 if w["kind"] == "wave2d" else 2)
+        if w["kind"] == "wave2d":
+            return 4 * ((m * m + 8 * m) + 3 * m * m)
+        chains = w["iters_per_step"] // 2
+        chains -= chains % 2
+        b_writes = 8 * m * m if not temporal.SKIP_MID_B else 8 * m * m / max(1, chains)
+        return int(8 * ((m * m + 4 * m) + m * m) + b_writes)
     if kind != "tb":
         return bytes_per_iter(w)
     from paper_2512_19851_b200 import temporal
@@ -369,7 +384,7 @@ def run_reference_arm(args, w):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    if w["kind"] == "laplace":
+    if w["kind"] == "laplace" and w["n"] <= 2048:  # the reference runtime at C1 size (lap16k: minutes per step)
         workers = 1
         while workers * 2 <= min(8, host_threads()):
             workers *= 2
@@ -709,8 +724,8 @@ def main():
     # chain covers K nodes), so achieved = covered bytes / summed kernel time
     sweeps = dom[1]
     ev_steps = args.steps if inline_timing else 2
-    tb_sweeps = sum(len(v) * k for (kind, k), v in by_tag.items() if kind in ("tb", "res", "rsm"))
-    covered = len(kt) * sweeps if dom[0] in ("tb", "res", "rsm") else ev_steps * w["iters_per_step"] - tb_sweeps
+    tb_sweeps = sum(len(v) * k for (kind, k), v in by_tag.items() if kind in ("tb", "tc", "res", "rsm"))
+    covered = len(kt) * sweeps if dom[0] in ("tb", "tc", "res", "rsm") else ev_steps * w["iters_per_step"] - tb_sweeps
     logical_launches = max(1, covered // sweeps)
     bytes_launch = bytes_per_launch(w, dom)
     if world > 1:
@@ -727,7 +742,8 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            pkey = args.workload + {"tb": "_tb%d" % sweeps, "rsm": "_rsm%d" % sweeps}.get(dom[0], "")
+            pkey = args.workload + {"tb": "_tb%d" % sweeps, "tc": "_tc%d" % sweeps,
+                                    "rsm": "_rsm%d" % sweeps}.get(dom[0], "")
             traffic = json.load(open(prof)).get(pkey, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -749,6 +765,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": {"tb": "est_tb (K=%d fused sweeps)" % sweeps,
+                                "tc": "est_tc (%d fused sweeps, rank 2)" % sweeps,
                                 "res": "est_resident (%d sweeps)" % sweeps,
                                 "rsm": "est_resident_smem (%d sweeps)" % sweeps}.get(dom[0], "est_stream/est_node (1 sweep)"),
                      "sweeps_per_launch": sweeps,
@@ -767,7 +784,7 @@ def main():
                          "sweep_equivalent": {
                              "achieved": bytes_per_iter(w) // max(1, world) * sweeps / (mean_k / 1e3) / 1e9,
                              "frac": bytes_per_iter(w) // max(1, world) * sweeps / (mean_k / 1e3) / 1e9 / peak}}
-                        if dom[0] == "tb" else {})},
+                        if dom[0] in ("tb", "tc") else {})},
         "e2e": {"value": e2e_val, "unit": "GLUP/s",
                 "h2d_bytes_per_step": len(blob), "d2h_bytes_per_step": d2h,
                 "note": ("per step: the W_BATCH payload (DAG bytes) from host memory -> decode/analysis cache -> "

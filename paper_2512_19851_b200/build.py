@@ -94,6 +94,15 @@ def standard_sources() -> list:
                         for n in (1024, 512):  # the C4 / C2 bench layouts (depth 1)
                             xoff, py, pz = TileBuffer.pitches((n, n, n), (1, 1, 1), dt)
                             srcs.add(temporal.source(sig, dt, py=py, pz=pz, xoff=xoff)[0])
+                if rank == 2 and len(plan.statements) == 1:
+                    from . import temporal2d
+                    from .codegen import stmt_sig
+                    from .tiles import TileBuffer
+                    sig = stmt_sig(plan.statements[0], 2)
+                    if temporal2d.eligible(sig, dt):
+                        for n, d in ((16384, 2), (16384, 1)):  # the C3 wave / paper-shape Laplace layouts
+                            xoff, py, _pz = TileBuffer.pitches((n, n), (d, d), dt)
+                            srcs.add(temporal2d.source(sig, dt, py=py, xoff=xoff)[0])
     return sorted(srcs)
 
 

@@ -116,6 +116,8 @@ static int driver() {
 struct est_ctx {
     int device;
     cudaStream_t stream[2];
+    unsigned long long *hash_dev = nullptr;   // est_hash_box accumulator (allocated once)
+    unsigned long long *hash_host = nullptr;  // pinned result
 };
 struct est_module {
     CUmodule mod;
@@ -163,6 +165,8 @@ extern "C" int est_ctx_destroy(est_ctx *c) {
         cudaStreamSynchronize(c->stream[i]);
         cudaStreamDestroy(c->stream[i]);
     }
+    if (c->hash_dev) cudaFree(c->hash_dev);
+    if (c->hash_host) cudaFreeHost(c->hash_host);
     delete c;
     return 0;
 }
@@ -368,7 +372,16 @@ __global__ void __launch_bounds__(256) hash_box_kernel(est_box b, int64_t oz, in
         const int64_t z = r / b.ny, y = r - z * b.ny;
         const W *row = src + z * b.src_pz + y * b.src_py;
         const int64_t g0 = ((oz + z) * gy + (oy + y)) * gx + ox;
-        for (int64_t x = lane; x < b.nx; x += 32)
+        int64_t x = lane;
+        // four independent loads in flight per lane before the mixing
+        for (; x + 96 < b.nx; x += 128) {
+            const W v0 = row[x], v1 = row[x + 32], v2 = row[x + 64], v3 = row[x + 96];
+            acc += mix64((uint64_t)v0 + 0x9e3779b97f4a7c15ULL * (uint64_t)(g0 + x + 1));
+            acc += mix64((uint64_t)v1 + 0x9e3779b97f4a7c15ULL * (uint64_t)(g0 + x + 33));
+            acc += mix64((uint64_t)v2 + 0x9e3779b97f4a7c15ULL * (uint64_t)(g0 + x + 65));
+            acc += mix64((uint64_t)v3 + 0x9e3779b97f4a7c15ULL * (uint64_t)(g0 + x + 97));
+        }
+        for (; x < b.nx; x += 32)
             acc += mix64((uint64_t)row[x] + 0x9e3779b97f4a7c15ULL * (uint64_t)(g0 + x + 1));
     }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -381,23 +394,22 @@ extern "C" int est_hash_box(est_ctx *c, const est_box *b, const int64_t origin[3
     if (elem != 4 && elem != 8) return fail(14, "elem size %d unsupported", elem);
     if (b->nx * b->ny * b->nz <= 0) return 0;
     CUDA_TRY(cudaSetDevice(c->device));
-    unsigned long long *d = nullptr;
-    CUDA_TRY(cudaMallocAsync(&d, sizeof(*d), pick(c, 0)));
-    CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(*d), pick(c, 0)));
+    if (!c->hash_dev) CUDA_TRY(cudaMalloc(&c->hash_dev, sizeof(*c->hash_dev)));
+    if (!c->hash_host) CUDA_TRY(cudaMallocHost(&c->hash_host, sizeof(*c->hash_host)));
+    CUDA_TRY(cudaMemsetAsync(c->hash_dev, 0, sizeof(*c->hash_dev), pick(c, 0)));
     int64_t rows = b->ny * b->nz, blocks = (rows + 7) / 8;
     if (blocks > 8 * 148) blocks = 8 * 148;
     if (elem == 8)
         hash_box_kernel<unsigned long long><<<(unsigned)blocks, 256, 0, pick(c, 0)>>>(
-            *b, origin[0], origin[1], origin[2], gdims[1], gdims[2], d);
+            *b, origin[0], origin[1], origin[2], gdims[1], gdims[2], c->hash_dev);
     else
         hash_box_kernel<unsigned int><<<(unsigned)blocks, 256, 0, pick(c, 0)>>>(
-            *b, origin[0], origin[1], origin[2], gdims[1], gdims[2], d);
+            *b, origin[0], origin[1], origin[2], gdims[1], gdims[2], c->hash_dev);
     CUDA_TRY(cudaGetLastError());
-    unsigned long long h = 0;
-    CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, pick(c, 0)));
-    CUDA_TRY(cudaFreeAsync(d, pick(c, 0)));
+    CUDA_TRY(cudaMemcpyAsync(c->hash_host, c->hash_dev, sizeof(*c->hash_host), cudaMemcpyDeviceToHost,
+                             pick(c, 0)));
     CUDA_TRY(cudaStreamSynchronize(pick(c, 0)));
-    *out = h;
+    *out = *c->hash_host;
     return 0;
 }
 

@@ -27,7 +27,7 @@ import os
 import time
 from dataclasses import dataclass, field
 
-from . import codegen, resident, stream, temporal
+from . import codegen, resident, stream, temporal, temporal2d
 from .analysis import KernelPlan, analyze_dag, compile_plan, plan_key
 from .device import COMPUTE
 from .errors import MalformedDag
@@ -96,6 +96,7 @@ class GpuExecutor:
         self.resident_smem = resident.SMEM_ENABLED  # small rank-2 chains held in shared memory
         self._bar = 0                     # grid-barrier counter of the resident-smem skeleton
         self.tb_cfg = temporal.DEFAULT
+        self.tc_cfg = temporal2d.DEFAULT
         self._tb_sched: dict = {}
         self._in_twin: dict = {}     # array -> its current values live in the twin buffers (mid-run)
         self._dirty: dict = {}       # array -> epoch whose ghost round was virtual (computed in-chain)
@@ -328,6 +329,8 @@ class GpuExecutor:
                     self.exchanges.finish_pending()
                 if chain[0] == "lead":
                     self._launch_tb(node, plan, chain[1], key, chain[2])
+                elif chain[0] == "tc":
+                    self._launch_tc(node, plan, chain, key)
                 elif chain[0] == "rsm":
                     self._launch_resident_smem(node, plan, chain[1], key)
             elif pending and set(pending) & set(meta.array_max_offset) and self.overlap_eligible(plan):
@@ -347,7 +350,7 @@ class GpuExecutor:
             for a in sorted(node.writes):
                 self.store.bump_local_epoch(a)
             for a, e in pushes.get(node.node_id, ()):
-                virtual = chain is not None and chain[0] in ("lead", "member") and self._chain_reads(tb, node, a)
+                virtual = chain is not None and chain[0] in ("lead", "tc", "member") and self._chain_reads(tb, node, a)
                 self._round(a, e, defer=self.overlap and self.transport is not None, virtual=virtual)
             stats.nodes_executed += 1
             stats.node_ms[node.node_id] = (time.perf_counter() - t_node) * 1e3
@@ -437,7 +440,7 @@ class GpuExecutor:
                 or (not multi and len(self.store.tiles) != 1)):
             return {}
         phys = phys if phys is not None else self.store.phys_depth
-        ck = ((key, self.store.version, self.tb_cfg, self.temporal, self.resident_smem,
+        ck = ((key, self.store.version, self.tb_cfg, self.tc_cfg, self.temporal, self.resident_smem,
                tuple(sorted(phys.items())), multi) if key is not None else None)
         hit = self._tb_sched.get(ck) if ck is not None else None
         if hit is not None:
@@ -462,6 +465,13 @@ class GpuExecutor:
                 sched[dag.nodes[i].node_id] = ("rsm", j - i)
                 for q in range(i + 1, j):
                     sched[dag.nodes[q].node_id] = ("member",)
+            elif (not multi and c[4] == 2 and j - i >= 2 and self._tc_ok(sig, c)):
+                m = (j - i) // 2
+                m -= m % 2  # an even number of chains: A ends in its own buffers
+                for ch in range(m):
+                    lead = i + 2 * ch
+                    sched[dag.nodes[lead].node_id] = ("tc", ch, ch == m - 1, (c[0],))
+                    sched[dag.nodes[lead + 1].node_id] = ("member",)
             elif (self.temporal and c[4] == 3 and temporal.eligible(sig, c[5], self.tb_cfg)
                   and _volume(c[2]) // n_tiles >= temporal.MIN_POINTS
                   and (not multi or phys.get(c[0], (0,))[0] >= K * temporal.slot_radius(sig)[0][0])):
@@ -473,11 +483,151 @@ class GpuExecutor:
                     for q in range(1, K):
                         sched[dag.nodes[lead + q].node_id] = ("member",)
             i = j
+        if not multi and self.temporal and temporal2d.ENABLED:
+            self._schedule_rotations(dag, plans, phys, sched)
         if ck is not None:
             if len(self._tb_sched) > 256:
                 self._tb_sched.clear()
             self._tb_sched[ck] = sched
         return sched
+
+    def _tc_ok(self, sig, c) -> bool:
+        """Rank-2 two-sweep chain (temporal2d.py) for this run's statement."""
+        return (self.temporal and temporal2d.ENABLED and temporal2d.eligible(sig, c[5], self.tc_cfg)
+                and _volume(c[2]) >= temporal2d.MIN_POINTS)
+
+    def _rotation_candidate(self, plan, phys):
+        """(Q, P, X1, output bounds, plan key, dtype, sig) for a rank-2 node
+        `X1[S] = f(Q[S + o], P[S])` (temporal2d.roles), else None."""
+        if len(plan.statements) != 1:
+            return None
+        ps = plan.statements[0]
+        if len(ps.inputs) != 2:
+            return None
+        arrs = [self.store.arrays.get(x) for x in (*ps.inputs, ps.output)]
+        if any(x is None or x.rank != 2 for x in arrs) or len({(x.shape, x.dtype) for x in arrs}) != 1:
+            return None
+        if len({ps.output, *ps.inputs}) != 3:
+            return None
+        if len({phys.get(x, self.depths.get(x)) for x in (*ps.inputs, ps.output)}) != 1:
+            return None
+        sig = codegen.stmt_sig(ps, 2)
+        r = temporal2d.roles(sig)
+        if r is None or r[1] is None:
+            return None
+        return (ps.inputs[r[0]], ps.inputs[r[1]], ps.output, tuple(ps.output_slice_bounds),
+                plan_key(ps.instructions), arrs[0].dtype, sig)
+
+    def _schedule_rotations(self, dag, plans, phys, sched: dict) -> None:
+        """Runs of rank-2 rotation nodes (node k+1 = f(X1_k stencil, Q_k
+        centre) -> P_k, the wave's u2 = f(u1, u0) time stepping) become
+        two-sweep tc chains. The step-2 array of each chain is written into
+        its other buffer; every array of the run gets a twin."""
+        cand = [None if dag.nodes[k].node_id in sched else self._rotation_candidate(p, phys)
+                for k, p in enumerate(plans)]
+        i, n = 0, len(cand)
+        while i < n:
+            c = cand[i]
+            if c is None or not (temporal2d.eligible(c[6], c[5], self.tc_cfg)
+                                 and _volume(c[3]) >= temporal2d.MIN_POINTS):
+                i += 1
+                continue
+            j = i + 1
+            while (j < n and cand[j] is not None and cand[j][3:6] == c[3:6]
+                   and cand[j][0] == cand[j - 1][2] and cand[j][1] == cand[j - 1][0]
+                   and cand[j][2] == cand[j - 1][1]):
+                j += 1
+            m = (j - i) // 2
+            arrays = (c[0], c[1], c[2])
+            for ch in range(m):
+                lead = i + 2 * ch
+                sched[dag.nodes[lead].node_id] = ("tc", ch, ch == m - 1, arrays)
+                sched[dag.nodes[lead + 1].node_id] = ("member",)
+            i = j
+
+    def _launch_tc(self, node, plan, ent, key) -> None:
+        """One two-sweep rank-2 chain (temporal2d.py) on the single tile. The
+        step-2 array goes into its other buffer (home <-> twin); a run's last
+        chain copies every array that ends in its twin back home (S only:
+        outside S both buffers hold the same values since the run started)."""
+        _kind, ch, last, arrays = ent
+        ps = plan.statements[0]
+        state = tuple(self._in_twin.get(x, False) for x in arrays)
+        ck = (key, node.node_id, self.store.version, "tc", state) if key is not None else None
+        rec = self._launches.get(ck) if ck is not None else None
+        if rec is None or self.time_kernels:
+            self._recording = [] if ck is not None else None
+            try:
+                self._launch_tc_tile(ps, ch, last, arrays)
+            finally:
+                rec, self._recording = self._recording, None
+            if ck is not None and rec is not None:
+                self._launches[ck] = rec
+        else:
+            for kern, grid, params, coop in rec:
+                if kern is None:
+                    self.dev.copy_boxes(grid, params)
+                else:
+                    self.dev.launch(kern, grid, params, COMPUTE, self.transport is None, coop)
+        sig = codegen.stmt_sig(ps, 2)
+        sten, cen = temporal2d.roles(sig)
+        x2 = ps.inputs[cen] if cen is not None else ps.inputs[sten]
+        self._in_twin[x2] = not self._in_twin.get(x2, False)
+        if last:
+            for x in arrays:
+                self._in_twin[x] = False
+
+    def _launch_tc_tile(self, ps, ch: int, last: bool, arrays) -> None:
+        from ._lib import EstBox
+
+        sig = codegen.stmt_sig(ps, 2)
+        sten, cen = temporal2d.roles(sig)
+        q, x1 = ps.inputs[sten], ps.output
+        p = ps.inputs[cen] if cen is not None else None
+        x2 = p if p is not None else q
+        tile = next(iter(self.store.tiles.values()))
+        home = {x: tile.buffers[x] for x in arrays + (x1,)}
+        twin = {x: self.store.twins[(tile.coords, x)] for x in arrays}
+        ref = home[q]
+        d = ref.depth
+        s_lo = tuple(lo + dd for (lo, _hi), dd in zip(ps.output_slice_bounds, d[1:]))
+        s_hi = tuple(hi + dd for (_lo, hi), dd in zip(ps.output_slice_bounds, d[1:]))
+
+        def cur(x):
+            return twin[x] if self._in_twin.get(x, False) else home[x]
+
+        def box3(lo, hi):
+            return (0,) + tuple(lo), (1,) + tuple(hi)
+
+        if ch == 0:
+            for x in arrays:
+                boxes = temporal.complement_boxes(home[x], home[x].ptr, twin[x].ptr, *box3(s_lo, s_hi))
+                self.dev.copy_boxes(boxes, home[x].elem)
+                if self._recording is not None:
+                    self._recording.append((None, boxes, home[x].elem, False))
+        info = self.store.arrays[q]
+        src, name, block, smem, lay = temporal2d.source(sig, info.dtype, self.tc_cfg, py=ref.py, xoff=ref.xoff)
+        kern = self.dev.kernel(src, name, block, smem)
+        geo = temporal2d.item_geometry(s_lo, s_hi, lay, xoff=ref.xoff)
+        tq = self._tmap(cur(q), (lay["w0"], lay["rb"], 1), self.tc_cfg.l2promo)
+        tp = self._tmap(cur(p), (lay["w0"], lay["rb"], 1), self.tc_cfg.l2promo) if p is not None else tq
+        org = ref.xoff * ref.elem
+        other = home[x2] if self._in_twin.get(x2, False) else twin[x2]
+        npy, npx = ref.pz // ref.py, ref.ext[2] + 2 * ref.depth[2]
+        params = temporal2d.pack_params(tq, tp, cur(x1).ptr + org, other.ptr + org, npy, npx, s_lo, s_hi, geo,
+                                        write_x1=p is not None or last or not temporal.SKIP_MID_B)
+        self._launch(kern, (geo["blocks"], 1, 1), params, tag=("tc", 2))
+        if last:
+            ends = dict(self._in_twin)
+            ends[x2] = not ends.get(x2, False)
+            for x in arrays:
+                if ends.get(x, False):
+                    n = (s_hi[1] - s_lo[1], s_hi[0] - s_lo[0], 1)
+                    off = (ref.xoff + s_lo[0] * ref.py + s_lo[1]) * ref.elem
+                    boxes = [EstBox(twin[x].ptr + off, home[x].ptr + off, ref.py, ref.pz, ref.py, ref.pz, *n)]
+                    self.dev.copy_boxes(boxes, ref.elem)
+                    if self._recording is not None:
+                        self._recording.append((None, boxes, ref.elem, False))
 
     def _chain_reads(self, tb, node, a) -> bool:
         """The round of array `a` pushed after chain node `node` is consumed
@@ -502,6 +652,8 @@ class GpuExecutor:
         for ent in sched.values():
             if ent[0] == "lead":
                 want.add(ent[3])
+            elif ent[0] == "tc":
+                want.update(ent[3])
         out = []
         for a in sorted(want):
             sig = (self.store.arrays[a], phys.get(a, self.depths.get(a)), self.store.version)
