@@ -483,7 +483,7 @@ class GpuExecutor:
                     for q in range(1, K):
                         sched[dag.nodes[lead + q].node_id] = ("member",)
             i = j
-        if not multi and self.temporal and temporal2d.ENABLED:
+        if not multi and self.temporal and temporal2d.ENABLED and temporal2d.ROTATIONS:
             self._schedule_rotations(dag, plans, phys, sched)
         if ck is not None:
             if len(self._tb_sched) > 256:

@@ -30,9 +30,12 @@ Kernel (one CTA per work item, several CTAs per SM):
 * compute thread c owns one 16-byte vector column (fp32 quads, fp64 pairs)
   of the step-1 frame. Its y-neighbours of both steps live in registers
   (windows of RB + 2*ry rows), x-neighbours come from shared memory: the Q
-  stage for step 1, a ring of step-1 rows (2*RB + ry rows) for step 2;
+  stage for step 1, a ring of step-1 rows (three banks of RB rows: written
+  by this stage, read back by this stage and the next) for step 2;
 * per stage: step 1 for RB rows (row t - ry of input row t), one named
   barrier, step 2 for RB rows (row t - 2*ry), so one barrier per RB rows;
+  interior stages of items inside S in x run a variant without row / column
+  checks;
 * step-1 rows / columns outside S take the intermediate array's stored value
   (the state of node-by-node execution); stores: X1 in place at S (a
   ping-pong skips it except in a run's last chain), the step-2 array into its
@@ -57,12 +60,12 @@ SMEM_PER_SM = 228 * 1024
 @dataclass(frozen=True)
 class TcCfg:
     bx: int = 0          # output columns per item (0: the widest whose TMA box fits 256)
-    rb: int = 0          # rows per stage (0: 2*ry + 1)
-    prefetch: int = 2    # stages in flight beyond the two being read
+    rb: int = 0          # rows per stage (0: auto, 2*ry + 1 and at least 4 for ping-pong)
+    prefetch: int = 1    # stages in flight beyond the two being read
     ychunk: int = 512    # target rows per item (chunks are balanced)
     min_items: int = 2048
     l2promo: int = 2
-    vec: int = 16        # bytes per thread vector (8: fp32 pairs, twice the threads per item)
+    vec: int = 0         # bytes per thread vector (0: auto, 8 = fp32 pairs for rotations, else 16)
 
 
 def _env_cfg() -> TcCfg:
@@ -76,6 +79,10 @@ def _env_cfg() -> TcCfg:
 
 DEFAULT = _env_cfg()
 ENABLED = os.environ.get("EST_TC", "1") == "1"
+# rotation chains (the wave) are correct but lose to single sweeps at C3
+# (523 vs 548 GLUP/s: the single-sweep kernel already moves 12 B/LUP at the
+# copy roofline, the chain's 8 B/LUP run at ~4.2 TB/s); opt-in
+ROTATIONS = os.environ.get("EST_TC_ROT", "0") == "1"
 # chains are scheduled from this many output points (below: the single-sweep
 # stream kernel or the shared-memory-resident chain)
 MIN_POINTS = int(os.environ.get("EST_TC_MIN_POINTS", 1 << 24))
@@ -119,13 +126,14 @@ def layout(st: StmtSig, dtype: int, cfg: TcCfg) -> dict:
     sten, cen = roles(st)
     _rz, ry, rx = slot_radius(st)[sten]
     elem = ELEM[dtype]
-    V = max(2, cfg.vec // elem)
+    vec = cfg.vec or (8 if (cen is not None and elem == 4) else 16)
+    V = max(2, vec // elem)
     A = 16 // elem  # TMA boxes must start on a 16-byte aligned column
     m1 = _round(rx, V)
     m0 = _round(m1 + rx, A)
     bx = cfg.bx or (256 - 2 * m0) // A * A
     W0, W1 = bx + 2 * m0, bx + 2 * m1
-    RB = cfg.rb or (2 * ry + 1)
+    RB = cfg.rb or (2 * ry + 1 if cen is not None else max(2 * ry + 1, 4))
     RB = max(RB, ry)
     P1 = W1 // V
     NT = _round(P1, 32)
@@ -135,7 +143,7 @@ def layout(st: StmtSig, dtype: int, cfg: TcCfg) -> dict:
     # have the same inner extent, a multiple of 32 bytes
     pb = _round(RB * W0 * elem, 128) if cen is not None else 0
     stage = qb + pb
-    C1 = 2 * RB + ry
+    C1 = 3 * RB  # three banks of RB step-1 rows (this stage, the previous, the next)
     W1p = W1 + 2 * V
     ring1 = S0 * stage
     data = _round(ring1 + C1 * W1p * elem, 8)
@@ -206,6 +214,91 @@ class _Emitter:
             for c in sorted(comps):
                 self.a(f"{ind}const {self.T} n{step}{side}{i}_{c} = nv{step}{side}{i}.{'xyzw'[c]};")
 
+    def emit_stage(self, ind: str, fast: bool) -> None:
+        """One stage: step 1 for RB rows, the named barrier, step 2 for RB rows.
+        The fast variant (interior stages of items inside S in x) has no row
+        or column checks."""
+        lay, a = self.lay, self.a
+        V, ry, RB, NT = lay["V"], lay["ry"], lay["rb"], lay["nt"]
+        W0, W1p = lay["w0"], lay["w1p"]
+        rot = lay["cen"] is not None
+        PY, VT, T = self.py, self.VT, self.T
+        a(f"{ind}const long long r1 = (long long)(ys - {3 * ry} + tb) * {PY} + gx;  // step-1 row of unroll 0")
+        for i in range(RB):
+            i3 = ind + "  "
+            a(f"{ind}{{  // step 1, unroll {i}: input row t = tb + {i}, step-1 row t - {ry}")
+            a(f"{i3}{{ const {VT} v = *reinterpret_cast<const {VT}*>(QS + {i * W0}); "
+              + " ".join(f"q{2 * ry + i}_{v} = v.{'xyzw'[v]};" for v in range(V)) + " }")
+            if rot:
+                a(f"{i3}const {VT} pv{i} = *reinterpret_cast<const {VT}*>(PS + {i * W0});")
+                for v in range(V):
+                    a(f"{i3}const T p{i}_{v} = pv{i}.{'xyzw'[v]};")
+            need: dict = {}
+            bodies = [self._expr(1, i, v, need) for v in range(V)]
+            # x-neighbours of step 1 at row t - ry: this stage's row i - ry or the previous stage's
+            src_row = i - ry
+            base = f"(QS + {src_row * W0})" if src_row >= 0 else f"(QP + {(src_row + RB) * W0})"
+            out = [f"x{2 * ry + i}_{v}" for v in range(V)]
+            vec = f"make_{VT}({', '.join(out)})"
+            if fast:
+                self._nbr_loads(i3, 1, i, need, base)
+                for v, (lines, res) in enumerate(bodies):
+                    a(f"{i3}{{ " + " ".join(lines) + f" {out[v]} = {res}; }}")
+                a(f"{i3}*reinterpret_cast<{VT}*>(WB + {i * W1p}) = {vec};")
+                a(f"{i3}if (p.wb && own) *reinterpret_cast<{VT}*>(x1m + r1 + {i * PY}) = {vec};")
+                a(f"{ind}}}")
+                continue
+            a(f"{i3}const int t = tb + {i};")
+            a(f"{i3}if (t >= {2 * ry} && t < n0) {{")
+            i4 = i3 + "  "
+            i5 = i4 + "  "
+            a(f"{i4}const int u1 = ys - {3 * ry} + t;  // padded row of this step-1 row")
+            a(f"{i4}if (u1 >= p.sy0 && u1 < p.sy1) {{")
+            self._nbr_loads(i5, 1, i, need, base)
+            for v, (lines, res) in enumerate(bodies):
+                a(f"{i5}{{ " + " ".join(lines) + f" {out[v]} = {res}; }}")
+            a(f"{i5}if (!xin) {{")
+            for v in range(V):
+                a(f"{i5}  if (!xs{v}) {out[v]} = xp{v} ? x1m[r1 + {i * PY + v}] : (T)0;")
+            a(f"{i5}}}")
+            a(f"{i4}}} else {{  // row outside S: the stored value (0 beyond the padded box)")
+            a(f"{i5}const bool yp = u1 >= 0 && u1 < p.npy;")
+            for v in range(V):
+                a(f"{i5}{out[v]} = (yp && xp{v}) ? x1m[r1 + {i * PY + v}] : (T)0;")
+            a(f"{i4}}}")
+            a(f"{i4}*reinterpret_cast<{VT}*>(WB + {i * W1p}) = {vec};")
+            a(f"{i4}if (p.wb && own && u1 >= ys && u1 < ys + nyl) {{")
+            a(f"{i5}T* dst = x1m + r1 + {i * PY};")
+            a(f"{i5}if (xin) *reinterpret_cast<{VT}*>(dst) = {vec};")
+            a(f"{i5}else {{ " + " ".join(f"if (xs{v}) dst[{v}] = {out[v]};" for v in range(V)) + " }")
+            a(f"{i4}}}")
+            a(f"{i3}}}")
+            a(f"{ind}}}")
+        a(f"{ind}asm volatile(\"bar.sync 1, {NT};\" ::: \"memory\");")
+        a(f"{ind}if (tid == 0) {{ if (s > 0) mbar_arrive(empty + prv); if (s == nst - 1) mbar_arrive(empty + stg); }}")
+        a(f"{ind}const long long r2 = r1 - {ry * PY};  // step-2 row of unroll 0")
+        for i in range(RB):
+            i3 = ind + "  "
+            cond = "" if fast else f"if (tb + {i} >= {4 * ry} && tb + {i} < n0) "
+            a(f"{ind}{cond}{{  // step 2, unroll {i}: row t - {2 * ry}")
+            src = f"(WB + {(i - ry) * W1p})" if i >= ry else f"(WP + {(RB + i - ry) * W1p})"
+            a(f"{i3}const T* R = {src};")
+            need = {}
+            bodies = [self._expr(2, i, v, need) for v in range(V)]
+            self._nbr_loads(i3, 2, i, need, "R")
+            for v, (lines, res) in enumerate(bodies):
+                a(f"{i3}T o{v}; {{ " + " ".join(lines) + f" o{v} = {res}; }}")
+            ov = f"make_{VT}({', '.join(f'o{v}' for v in range(V))})"
+            if fast:
+                a(f"{i3}if (own) *reinterpret_cast<{VT}*>(x2m + r2 + {i * PY}) = {ov};")
+            else:
+                a(f"{i3}if (own) {{")
+                a(f"{i3}  T* dst = x2m + r2 + {i * PY};")
+                a(f"{i3}  if (xin) *reinterpret_cast<{VT}*>(dst) = {ov};")
+                a(f"{i3}  else {{ " + " ".join(f"if (xs{v}) dst[{v}] = o{v};" for v in range(V)) + " }")
+                a(f"{i3}}}")
+            a(f"{ind}}}")
+
     def source(self) -> str:
         lay, a = self.lay, self.a
         cfg = lay["cfg"]
@@ -213,10 +306,14 @@ class _Emitter:
         W0, W1, W1p, P1, NT, E = lay["w0"], lay["w1"], lay["w1p"], lay["p1"], lay["nt"], lay["elem"]
         m0, m1, BX = lay["m0"], lay["m1"], lay["bx"]
         rot = lay["cen"] is not None
+        tmap_p = rot
         PY, VT, T = self.py, self.VT, self.T
         NW = NT // 32
         H = RB + 2 * ry  # register window rows
-        minb = blocks_per_sm(lay)
+        # the min-blocks hint caps the registers per thread: at most 4 so the
+        # register windows are not spilled (the hardware still runs more CTAs
+        # per SM when registers and shared memory allow)
+        minb = min(blocks_per_sm(lay), 4)
         lay["min_blocks"] = minb
         a(f'// generated by paper_2512_19851_b200/temporal2d.py - skeleton "tc" (2 fused sweeps, rank 2, '
           f'{"rotation" if rot else "ping-pong"}) {cfg} bx={BX} rb={RB} py={PY} xoff={self.xoff}')
@@ -252,15 +349,15 @@ class _Emitter:
         a(f"  if (warp == {NW}) {{")
         a("    if ((tid & 31) != 0) return;")
         a("    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tq) : \"memory\");")
-        if rot:
+        if tmap_p:
             a("    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tp) : \"memory\");")
         a("    for (int s = 0; s < nst; ++s) {")
         a(f"      const int stg = s % {S0};")
         a(f"      if (s >= {S0}) mbar_wait(empty + stg, ((s / {S0}) - 1) & 1);")
-        a(f"      mbar_expect(full + stg, {RB * W0 * E * (2 if rot else 1)});")
+        a(f"      mbar_expect(full + stg, {RB * W0 * E * (2 if tmap_p else 1)});")
         a(f"      unsigned char* sb = smem + stg * {lay['stage']};")
         a(f"      tma_load3(sb, &p.tq, x0 + {self.xoff - m0}, ys - {2 * ry} + s * {RB}, 0, full + stg);")
-        if rot:
+        if tmap_p:
             a(f"      tma_load3(sb + {lay['qb']}, &p.tp, x0 + {self.xoff - m0}, ys - {3 * ry} + s * {RB}, 0, full + stg);")
         a("    }")
         a("    return;")
@@ -280,85 +377,32 @@ class _Emitter:
         for k in range(H):
             a(f"  T {', '.join(f'q{k}_{v} = 0' for v in range(V))};")
             a(f"  T {', '.join(f'x{k}_{v} = 0' for v in range(V))};")
-        a("  int stg = 0, ph = 0, prv = 0, r1b = 0;  // stage slot / phase, previous slot, ring row of t = s*RB")
+        a("  int stg = 0, ph = 0, prv = 0, bk = 0, bp = 2;  // stage slot / phase, previous slot, ring banks")
+        a(f"  const bool xfast = (x0 - {m1} >= p.sx0) && (x0 + {BX + m1} <= p.sx1);  // frame inside S in x")
         a("  for (int s = 0; s < nst; ++s) {")
         i2 = "    "
         a(f"{i2}const int tb = s * {RB};")
         a(f"{i2}mbar_wait(full + stg, ph);")
         a(f"{i2}const T* QS = reinterpret_cast<const T*>(smem + stg * {lay['stage']}) + {m0 - m1} + c * {V};")
         a(f"{i2}const T* QP = reinterpret_cast<const T*>(smem + prv * {lay['stage']}) + {m0 - m1} + c * {V};")
-        if rot:
+        if tmap_p:
             a(f"{i2}const T* PS = reinterpret_cast<const T*>(smem + stg * {lay['stage']} + {lay['qb']}) + {m0 - m1} + c * {V};")
-        # ---- step 1
-        for i in range(RB):
-            i3 = i2 + "  "
-            a(f"{i2}{{  // step 1, unroll {i}: input row t = tb + {i}, step-1 row t - {ry}")
-            a(f"{i3}const int t = tb + {i};")
-            a(f"{i3}{{ const {VT} v = *reinterpret_cast<const {VT}*>(QS + {i * W0}); "
-              + " ".join(f"q{2 * ry + i}_{v} = v.{'xyzw'[v]};" for v in range(V)) + " }")
-            if rot:
-                a(f"{i3}const {VT} pv{i} = *reinterpret_cast<const {VT}*>(PS + {i * W0});")
-                for v in range(V):
-                    a(f"{i3}const T p{i}_{v} = pv{i}.{'xyzw'[v]};")
-            a(f"{i3}if (t >= {2 * ry} && t < n0) {{")
-            i4 = i3 + "  "
-            a(f"{i4}const int u1 = ys - {3 * ry} + t;  // padded row of this step-1 row")
-            a(f"{i4}int rs = r1b + {i}; if (rs >= {C1}) rs -= {C1};")
-            a(f"{i4}T* W = ring1 + rs * {W1p};")
-            a(f"{i4}if (u1 >= p.sy0 && u1 < p.sy1) {{")
-            i5 = i4 + "  "
-            need: dict = {}
-            bodies = [self._expr(1, i, v, need) for v in range(V)]
-            # x-neighbours of step 1 at row t - ry: this stage's row i - ry or the previous stage's
-            src_row = i - ry
-            base = f"QS + {src_row * W0}" if src_row >= 0 else f"QP + {(src_row + RB) * W0}"
-            self._nbr_loads(i5, 1, i, need, f"({base})")
-            for v, (lines, res) in enumerate(bodies):
-                a(f"{i5}{{ " + " ".join(lines) + f" x{2 * ry + i}_{v} = {res}; }}")
-            a(f"{i5}if (!xin) {{")
-            for v in range(V):
-                a(f"{i5}  if (!xs{v}) x{2 * ry + i}_{v} = xp{v} ? x1m[(long long)u1 * {PY} + gx + {v}] : (T)0;")
-            a(f"{i5}}}")
-            a(f"{i4}}} else {{  // row outside S: the stored value (0 beyond the padded box)")
-            a(f"{i5}const bool yp = u1 >= 0 && u1 < p.npy;")
-            for v in range(V):
-                a(f"{i5}x{2 * ry + i}_{v} = (yp && xp{v}) ? x1m[(long long)u1 * {PY} + gx + {v}] : (T)0;")
-            a(f"{i4}}}")
-            vec = f"make_{VT}({', '.join(f'x{2 * ry + i}_{v}' for v in range(V))})"
-            a(f"{i4}*reinterpret_cast<{VT}*>(W) = {vec};")
-            a(f"{i4}if (p.wb && own && u1 >= ys && u1 < ys + nyl) {{")
-            a(f"{i5}T* dst = x1m + (long long)u1 * {PY} + gx;")
-            a(f"{i5}if (xin) *reinterpret_cast<{VT}*>(dst) = {vec};")
-            a(f"{i5}else {{ " + " ".join(f"if (xs{v}) dst[{v}] = x{2 * ry + i}_{v};" for v in range(V)) + " }")
-            a(f"{i4}}}")
-            a(f"{i3}}}")
-            a(f"{i2}}}")
-        a(f"{i2}asm volatile(\"bar.sync 1, {NT};\" ::: \"memory\");")
-        a(f"{i2}if (tid == 0) {{ if (s > 0) mbar_arrive(empty + prv); if (s == nst - 1) mbar_arrive(empty + stg); }}")
-        # ---- step 2
-        for i in range(RB):
-            i3 = i2 + "  "
-            a(f"{i2}if (tb + {i} >= {4 * ry} && tb + {i} < n0) {{  // step 2, unroll {i}: row t - {2 * ry}")
-            a(f"{i3}const int u2 = ys - {4 * ry} + tb + {i};")
-            a(f"{i3}int rs = r1b + {i - ry}; if (rs < 0) rs += {C1}; if (rs >= {C1}) rs -= {C1};")
-            a(f"{i3}const T* R = ring1 + rs * {W1p};")
-            need = {}
-            bodies = [self._expr(2, i, v, need) for v in range(V)]
-            self._nbr_loads(i3, 2, i, need, "R")
-            for v, (lines, res) in enumerate(bodies):
-                a(f"{i3}T o{v}; {{ " + " ".join(lines) + f" o{v} = {res}; }}")
-            a(f"{i3}if (own) {{")
-            a(f"{i3}  T* dst = x2m + (long long)u2 * {PY} + gx;")
-            a(f"{i3}  if (xin) *reinterpret_cast<{VT}*>(dst) = make_{VT}({', '.join(f'o{v}' for v in range(V))});")
-            a(f"{i3}  else {{ " + " ".join(f"if (xs{v}) dst[{v}] = o{v};" for v in range(V)) + " }")
-            a(f"{i3}}}")
-            a(f"{i2}}}")
+
+        a(f"{i2}T* WB = ring1 + bk * {RB * W1p};  // ring bank of this stage's step-1 rows")
+        a(f"{i2}const T* WP = ring1 + bp * {RB * W1p};  // ... and of the previous stage's")
+        # fast stage: every step-1 row lies in the item's own output rows (so
+        # inside S), every step-2 row is valid and the frame is inside S in x
+        a(f"{i2}if (xfast && tb >= {4 * ry} && tb + {RB} <= nyl + {3 * ry}) {{")
+        self.emit_stage(i2 + "  ", fast=True)
+        a(f"{i2}}} else {{")
+        self.emit_stage(i2 + "  ", fast=False)
+        a(f"{i2}}}")
         # ---- shift the register windows by RB rows
         for k in range(2 * ry):
             a(f"{i2}" + " ".join(f"q{k}_{v} = q{k + RB}_{v}; x{k}_{v} = x{k + RB}_{v};" for v in range(V)))
         a(f"{i2}prv = stg;")
         a(f"{i2}if (++stg == {S0}) {{ stg = 0; ph ^= 1; }}")
-        a(f"{i2}r1b += {RB}; if (r1b >= {C1}) r1b -= {C1};")
+        a(f"{i2}bp = bk; if (++bk == 3) bk = 0;")
         a("  }")
         a("}")
         return "\n".join(self.L) + "\n"

@@ -18,6 +18,8 @@ full size, and compares EVERY array with the strict-order C oracle
 * C3 — 2-D acoustic wave r=2 16384^2 fp32: one bench step (100 wave steps)
   against the fp32 strict route; bar: bit-equal (and within the north star's
   1e-5 relative tolerance, asserted separately so a failure says which).
+* lap16k — the paper's 2-D Laplace per-GPU shape, 16384^2 fp64 (est_tc
+  ping-pong chains), bench steps up to a CUDA-graph replay.
 
 Bar for fp64: bit-exact (NaNs compared as a class). Arrays are fetched and
 compared one at a time to bound host memory (C4: 3 x 8.6 GB resident).
@@ -139,5 +141,28 @@ def test_c3_16384_fp32_wave():
         job.run_bytes(blob)
         want = _oracle(prog, blob, 1)
         _compare_all(job, want, rtol=1e-5)
+    finally:
+        job.close()
+
+
+def test_lap16k_bench_steps_bit_exact_with_graph_replay():
+    """The paper's 2-D Laplace shape (16384^2 fp64, bench workload `lap16k`)
+    as bench.py runs it: two-sweep rank-2 chains (est_tc, B stored only by a
+    run's last chain), steps up to the first CUDA-graph replay."""
+    w = bench.WORKLOADS["lap16k"]
+    job, prog, arrays = bench.build_job(w, 1, 0)
+    try:
+        blob = bench.step_dag(w, prog.shapes, prog.dtypes, arrays)
+        ex = job.executors[0]
+        job.run_bytes(blob)
+        assert ex._scratch, "the default lap16k path did not run the rank-2 chain (est_tc)"
+        steps = 1
+        while ex.replays == 0 and steps < 5:
+            job.run_bytes(blob)
+            steps += 1
+        job.sync()
+        assert ex.replays == 1
+        want = _oracle(prog, blob, steps)
+        _compare_all(job, want)
     finally:
         job.close()

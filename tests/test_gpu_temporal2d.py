@@ -23,11 +23,18 @@ from paper_2512_19851_b200.wire import DTYPE_F32, DTYPE_F64, encode_dag
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def chains_at_test_sizes(monkeypatch):
+@pytest.fixture(autouse=True, params=["auto", "vec16"])
+def chains_at_test_sizes(request, monkeypatch):
+    """Every case runs with the default layout (8-byte vectors for fp32
+    rotations) and with 16-byte vectors everywhere."""
+    import dataclasses
+
     from paper_2512_19851_b200 import resident, temporal2d
+    if request.param == "vec16":
+        monkeypatch.setattr(temporal2d, "DEFAULT", dataclasses.replace(temporal2d.DEFAULT, vec=16))
     monkeypatch.setattr(temporal2d, "ENABLED", True)
     monkeypatch.setattr(temporal2d, "MIN_POINTS", 0)
+    monkeypatch.setattr(temporal2d, "ROTATIONS", True)  # opt-in by default (measured slower at C3)
     monkeypatch.setattr(resident, "SMEM_ENABLED", False)  # the small-grid chain has its own suite
 
 

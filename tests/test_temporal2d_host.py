@@ -20,6 +20,7 @@ from paper_2512_19851_b200.wire import DTYPE_F32, DTYPE_F64
 @pytest.fixture(autouse=True)
 def _small_grids_chain(monkeypatch):
     monkeypatch.setattr(temporal2d, "MIN_POINTS", 0)
+    monkeypatch.setattr(temporal2d, "ROTATIONS", True)  # opt-in by default (measured slower at C3)
 
 
 def _executor(shapes, dtypes=None, temporal_on=True):
