@@ -315,8 +315,8 @@ class GpuExecutor:
             plan = plans[node.node_id]
             if self.transport is not None:
                 writes = set(node.writes)
-                if chain is not None and chain[0] == "lead":
-                    writes |= set(plan.statements[0].inputs)  # the chain also writes A
+                if chain is not None and chain[0] in ("lead", "tc"):
+                    writes |= set(plan.statements[0].inputs)  # the chain also writes A (or P)
                 for a in sorted(writes):
                     self.transport.before_write(a)
             pending = self.exchanges.pending
@@ -465,7 +465,7 @@ class GpuExecutor:
                 sched[dag.nodes[i].node_id] = ("rsm", j - i)
                 for q in range(i + 1, j):
                     sched[dag.nodes[q].node_id] = ("member",)
-            elif (not multi and c[4] == 2 and j - i >= 2 and self._tc_ok(sig, c)):
+            elif (n_tiles == 1 and c[4] == 2 and j - i >= 2 and self._tc_ok(sig, c)):
                 m = (j - i) // 2
                 m -= m % 2  # an even number of chains: A ends in its own buffers
                 for ch in range(m):
@@ -483,7 +483,7 @@ class GpuExecutor:
                     for q in range(1, K):
                         sched[dag.nodes[lead + q].node_id] = ("member",)
             i = j
-        if not multi and self.temporal and temporal2d.ENABLED and temporal2d.ROTATIONS:
+        if n_tiles == 1 and self.temporal and temporal2d.ENABLED and temporal2d.ROTATIONS:
             self._schedule_rotations(dag, plans, phys, sched)
         if ck is not None:
             if len(self._tb_sched) > 256:
@@ -555,7 +555,9 @@ class GpuExecutor:
         state = tuple(self._in_twin.get(x, False) for x in arrays)
         ck = (key, node.node_id, self.store.version, "tc", state) if key is not None else None
         rec = self._launches.get(ck) if ck is not None else None
-        if rec is None or self.time_kernels:
+        if not self.store.tiles:
+            pass  # a worker without the (single) tile keeps the bookkeeping only
+        elif rec is None or self.time_kernels:
             self._recording = [] if ck is not None else None
             try:
                 self._launch_tc_tile(ps, ch, last, arrays)

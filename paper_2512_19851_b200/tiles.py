@@ -203,6 +203,7 @@ class GpuTileStore:
         self._epochs: dict = {}  # array -> local epoch (also valid with no tiles)
         self._ghosts: dict = {}
         self.phys_depth: dict = {}  # array -> allocated ghost frame (>= logical; also with no tiles)
+        self.logical_depth: dict = {}  # array -> job-wide logical ghost depth (also with no tiles)
         self.twins: dict = {}       # (coords, array) -> twin TileBuffer of a temporal chain's input
         self.twin_sig: dict = {}    # array -> (info, frame, store version) the twins were made for
 
@@ -243,6 +244,10 @@ class GpuTileStore:
         the caller bumps the local epoch as the reference does."""
         self.check_depth_fits(array, depth)
         rank = self.arrays[array].rank
+        # the job-wide logical depth: a worker that owns no tile sees the same
+        # growth (and bumps its epochs with everyone else)
+        old_logical = self.logical_depth.get(array, (0,) * rank)
+        self.logical_depth[array] = tuple(max(a, b) for a, b in zip(old_logical, depth))
         phys = tuple(max(a, b) for a, b in zip(depth, phys if phys is not None else depth))
         self.phys_depth[array] = tuple(max(a, b) for a, b in zip(self.phys_depth.get(array, phys), phys))
         grew = grew_buf = False
@@ -272,6 +277,8 @@ class GpuTileStore:
             grew_buf = True
         if grew_buf:
             self.version += 1
+        if not self.tiles:
+            return self.logical_depth[array] != old_logical
         return grew
 
     def fetch_dtype(self, array: int):

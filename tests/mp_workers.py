@@ -128,3 +128,38 @@ def migrate_rank(rank, world, kind, shrink_to):
            "epochs": {a: job.store.local_epoch(a) for a in prog.shapes}}
     job.close()
     return out
+
+
+def single_tile_chain_rank(rank, world, kind):
+    """A single-tile 2-D job whose worker owns a transport (the GPU worker
+    process, world 1 or a job whose other ranks own no tile): the rank-2
+    chain kernel (est_tc) runs there too. Returns the kernels launched by one
+    step and the arrays' final epochs."""
+    import paper_2512_19851_b200.ipc as ipc
+    from fakedev import FakeDevice
+    from paper_2512_19851_b200 import temporal2d
+    from paper_2512_19851_b200.programs import DagProgram, laplace_iteration_statements, laplace_program
+    from paper_2512_19851_b200.tiles import decompose
+    from paper_2512_19851_b200.wire import encode_dag
+
+    temporal2d.MIN_POINTS = 0
+    ipc.Device = lambda device=0: FakeDevice(device, tag=f"r{rank}")
+    prog = DagProgram()
+    laplace_program(prog, 64, 0)
+    decomp = decompose((64, 64), 1, 1)   # one tile, owned by rank 0
+    job = ipc.IpcGpuJob(rank, world, decomp=decomp, owner_map={c: 0 for c in decomp.all_coords()})
+    try:
+        for a in sorted(prog.shapes):
+            job.create_array(prog.shapes[a])
+        job.run(prog.dag)
+        step = DagProgram()
+        for a in sorted(prog.shapes):
+            step.builder.declare_array(a, prog.shapes[a])
+        laplace_iteration_statements(step, 0, 1, 8)
+        job.dev.log.clear()
+        job.run_bytes(encode_dag(step.dag))
+        names = [e[2] for e in job.dev.log if e[0] == "launch"]
+        return {"names": names, "epochs": {a: job.store.local_epoch(a) for a in sorted(prog.shapes)},
+                "tiles": len(job.store.tiles)}
+    finally:
+        job.close()

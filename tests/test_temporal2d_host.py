@@ -174,3 +174,18 @@ def test_roles_reject_unchainable():
         p.assign(c, box, expr)
         st = compile_plan(p.dag.nodes[0], p.dag.ast_table).statements[0]
         assert (temporal2d.roles(codegen.stmt_sig(st, 2)) is not None) == ok
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_chain_runs_in_worker_job_with_transport(world):
+    """The GPU worker process runs batches through an IPC job (a transport
+    exists even at world 1): a single-tile 2-D job still chains, and a rank
+    without the tile keeps the same epochs without launching."""
+    from mp_workers import single_tile_chain_rank
+    from paper_2512_19851_b200.ipc import spawn_local_job
+
+    res = spawn_local_job(world, single_tile_chain_rank, "laplace", timeout=300)
+    owner = [r for r in res if r["tiles"]]
+    assert len(owner) == 1 and owner[0]["names"].count("est_tc") == 4
+    assert len({tuple(sorted(r["epochs"].items())) for r in res}) == 1
+    assert all(not r["names"] for r in res if not r["tiles"])
