@@ -202,9 +202,14 @@ def owner_map_from_manifest(m: dict) -> dict:
     return owners
 
 
-def restore_tiles(job, manifest: dict) -> dict:
-    """Install this worker's tiles from the daemons; returns {array: depth}."""
+def restore_tiles(job, manifest: dict, stats: dict | None = None) -> dict:
+    """Install this worker's tiles from the daemons; returns {array: depth}.
+    `stats` (optional) receives the split: daemon requests, tile-buffer
+    allocation, daemon-arena IPC mapping, copies + sync, frees (ms)."""
+    import time
+
     store, dev = job.store, job.dev
+    st = {"daemon_ms": 0.0, "alloc_ms": 0.0, "map_ms": 0.0, "copy_ms": 0.0, "free_ms": 0.0, "bytes": 0}
     depths = {}
     for key, meta in manifest["arrays"].items():
         a = int(key)
@@ -220,34 +225,48 @@ def restore_tiles(job, manifest: dict) -> dict:
         for rec in manifest["allocations"]:
             if rec["owner"] != job.rank:
                 continue
+            t0 = time.perf_counter()
             cl = clients.get(rec["daemon"])
             if cl is None:
                 cl = clients[rec["daemon"]] = DaemonClient(rec["daemon"])
             handle, off, serial, meta = cl.dev_open(rec["alloc_id"])
+            st["daemon_ms"] += (time.perf_counter() - t0) * 1e3
             header = bytes.fromhex(meta["header"])
             a, coords, ext, depth, epoch, _hs = parse_blob_header(header)
             payload = int(np.prod(ext)) * (8 if int(meta.get("dtype", 0)) == 0 else 4)
             if len(header) + payload != rec["nbytes"]:
                 raise ValueError(f"allocation {rec['alloc_id']} size mismatch")
             tile = store.tiles.setdefault(tuple(coords), GpuTile(tuple(coords)))
+            t0 = time.perf_counter()
             buf = TileBuffer(dev, ext, depth, int(meta.get("dtype", 0)))
+            t1 = time.perf_counter()
             base = arenas.get((rec["daemon"], serial))
             if base is None:
                 base = arenas[(rec["daemon"], serial)] = dev.ipc_open(handle)
+            t2 = time.perf_counter()
+            st["alloc_ms"] += (t1 - t0) * 1e3
+            st["map_ms"] += (t2 - t1) * 1e3
+            st["bytes"] += payload
             opened.append((cl, rec["alloc_id"]))
             dev.copy_box(_interior_box(buf, base + off, False), buf.elem, COMPUTE)
             tile.buffers[a] = buf
             tile.depths[a] = tuple(depth)
             tile.local_epoch[a] = epoch
             tile.ghost_epoch[a] = epoch
+        t0 = time.perf_counter()
         dev.sync()
+        t1 = time.perf_counter()
         for base in arenas.values():
             dev.ipc_close(base)
         for cl, alloc_id in opened:
             cl.dev_free(alloc_id)
+        st["copy_ms"] += (t1 - t0) * 1e3
+        st["free_ms"] += (time.perf_counter() - t1) * 1e3
     finally:
         for cl in clients.values():
             cl.close()
     for a in sorted(store.arrays):
         store.bump_local_epoch(a)
+    if stats is not None:
+        stats.update({k: (round(v, 1) if isinstance(v, float) else v) for k, v in st.items()})
     return depths

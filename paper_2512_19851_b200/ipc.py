@@ -69,6 +69,9 @@ class SharedCounters:
 
 READY_OFF, PULLED_OFF = 0, 128  # byte offsets of the two flag words (separate 128-B lines)
 FLAGS_KEY = (("flags",), -1)     # buffer-table key of a rank's flag block
+# the halo arena: flags + halo windows, the only memory a halo neighbour maps
+HALO_ARENA = int(os.environ.get("EST_HALO_ARENA_BYTES", 64 << 20))
+WINDOWS = os.environ.get("EST_HALO_WINDOWS", "1") == "1"
 
 
 class IpcPeerTransport(LocalPeerTransport):
@@ -88,14 +91,20 @@ class IpcPeerTransport(LocalPeerTransport):
     never goes backwards."""
 
     def __init__(self, job: "IpcGpuJob"):
-        from .pool import device_alloc
+        from .pool import DevicePool
 
         self.job = job
         self.w = job.rank
         self.store = job.store
         self.dev = job.dev
         self.seq = 0
-        self.flags = device_alloc(self.dev, 256)  # [READY_OFF] ready, [PULLED_OFF] pulled; zeroed
+        # flags and the rank-3 halo windows live in their own small exported
+        # arena: halo neighbours map only that, never the GiB-sized tile arenas
+        self.hpool = DevicePool(self.dev, HALO_ARENA, grow=2)
+        self.flags = self.hpool.alloc(256)  # [READY_OFF] ready, [PULLED_OFF] pulled; zeroed
+        self.windows: dict = {}  # (coords, array) -> (ptr, signature): the slab's boundary planes
+        self.window_maps: set = set()  # peers' windows this rank has pulled from (introspection)
+        self._exports: dict = {}
         self.ready = [self.dev.event() for _ in range(RING)]   # intra-process: copy lane after compute
         self.pulled = [self.dev.event() for _ in range(RING)]  # intra-process: compute after copy lane
         self.peer_flag_base: dict = {}
@@ -132,9 +141,119 @@ class IpcPeerTransport(LocalPeerTransport):
             serial, handle, off = pool.locate(buf.ptr)
             out[(tuple(coords), ("twin", array))] = (serial, handle, off, buf.ext[3 - buf.rank:],
                                                       buf.depth[3 - buf.rank:], buf.dtype, buf.serial)
-        serial, handle, off = pool.locate(self.flags)
+        self._ensure_windows()
+        for (coords, array), (ptr, _sig) in self.windows.items():
+            serial, handle, off = self.hpool.locate(ptr)
+            out[(tuple(coords), ("win", array))] = (serial, handle, off, (), (), 0, ptr)
+        serial, handle, off = self.hpool.locate(self.flags)
         out[FLAGS_KEY] = (serial, handle, off, (), (), 0, 0)
         return out
+
+    # -- halo windows (rank-3 slabs) -----------------------------------------------
+    # A slab's neighbours read only its pd boundary planes on each side (pd =
+    # the array's physical z ghost depth). Before READY the owner copies those
+    # planes (from whichever buffer holds the array: home, or the temporal
+    # chain's twin mid-run) into a small window [lo: pd planes | hi: pd
+    # planes] in the halo arena, and the neighbours pull from the window. A
+    # restarted or re-mapped worker then maps a few MiB per neighbour instead
+    # of the neighbour's whole tile arena (~65 ms per GiB mapped,
+    # profiles/r2_c5_stage_split.md). The copy costs 2*pd planes per round
+    # (C4 on 8 GPUs: 32 MiB, ~10 us, against ~0.5 ms of chain compute).
+
+    @staticmethod
+    def _window_sig(buf) -> tuple:
+        return (buf.py, buf.pz, buf.xoff, tuple(buf.depth), tuple(buf.ext), buf.elem)
+
+    def _ensure_windows(self) -> None:
+        want = {}
+        if WINDOWS:
+            for coords, tile in self.store.tiles.items():
+                for a, buf in tile.buffers.items():
+                    if buf.rank == 3 and buf.depth[0] > 0:
+                        want[(tuple(coords), a)] = buf
+        for key in list(self.windows):
+            ptr, sig = self.windows[key]
+            if key not in want or sig != self._window_sig(want[key]):
+                self.hpool.free(ptr)
+                del self.windows[key]
+        for key, buf in sorted(want.items()):
+            if key not in self.windows:
+                nbytes = 2 * buf.depth[0] * buf.pz * buf.elem
+                self.windows[key] = (self.hpool.alloc(nbytes), self._window_sig(buf))
+        self._exports.clear()
+
+    def _window_box(self, buf, win: int, side: str, export: bool, dst_buf=None):
+        """Copy descriptor between a slab's boundary planes and a window
+        region: `side` "lo" = the first pd interior planes, "hi" = the last
+        pd. export: slab -> own window; else window (a peer's, mapped at
+        `win`) -> the ghost planes of `dst_buf` on the side facing it."""
+        from ._lib import EstBox
+
+        pd = buf.depth[0]
+        ez, ey, ex = buf.ext
+        inplane = (buf.xoff + buf.depth[1] * buf.py + buf.depth[2]) * buf.elem
+        region = win + (0 if side == "lo" else pd * buf.pz * buf.elem) + inplane
+        if export:
+            src = buf.interior_addr((0 if side == "lo" else ez - pd, 0, 0))
+            return EstBox(src, region, buf.py, buf.pz, buf.py, buf.pz, ex, ey, pd)
+        # the peer's lo planes fill our high ghost planes (it is our E
+        # neighbour), its hi planes our low ghost planes
+        gz = pd + ez if side == "lo" else 0
+        return EstBox(region, dst_buf.addr(gz, dst_buf.depth[1], dst_buf.depth[2]), buf.py, buf.pz,
+                      dst_buf.py, dst_buf.pz, ex, ey, pd)
+
+    def _export_boxes(self, array: int, twin: bool) -> list:
+        from .exchange import E, W, neighbour
+
+        ck = (array, self.store.version, id(self.job.owner_map), twin)
+        boxes = self._exports.get(ck)
+        if boxes is None:
+            boxes = []
+            owners = self.job.owner_map or {}
+            info = self.store.arrays[array]
+            for coords in sorted(self.store.tiles):
+                if (tuple(coords), array) not in self.windows:
+                    continue
+                buf = self.store.twins[(coords, array)] if twin else self.store.tiles[coords].buffers[array]
+                win = self.windows[(tuple(coords), array)][0]
+                for d, side in ((W, "lo"), (E, "hi")):
+                    nb = neighbour(self.store.decomp, info.rank, coords, d)
+                    if nb is not None and owners.get(nb, self.w) != self.w:
+                        boxes.append(self._window_box(buf, win, side, True))
+            if len(self._exports) > 256:
+                self._exports.clear()
+            self._exports[ck] = boxes
+        return boxes
+
+    def peer_window(self, owner: int, coords, array: int) -> int:
+        """Mapped address of `owner`'s halo window of (coords, array)."""
+        aserial, handle, off = self.peer_tables[(owner, tuple(coords), ("win", array))][:3]
+        self.window_maps.add((owner, tuple(coords), array))
+        base = self.arena_maps.get((owner, aserial))
+        if base is None:
+            base = self.arena_maps[(owner, aserial)] = self.dev.ipc_open(handle)
+        return base + off
+
+    def _uses_windows(self, array: int) -> bool:
+        return WINDOWS and self.store.arrays[array].rank == 3
+
+    def _pull_boxes(self, array: int, remote, twin: bool = False) -> list:
+        if not self._uses_windows(array):
+            return super()._pull_boxes(array, remote, twin)
+        from .exchange import E
+
+        ck = (array, self.store.version, self.peer_version, id(remote), twin, "win")
+        boxes = self._pulls.get(ck)
+        if boxes is None:
+            boxes = []
+            for coords, d, nb, owner in remote:
+                dst = self.store.twins[(coords, array)] if twin else self.store.tiles[coords].buffers[array]
+                win = self.peer_window(owner, nb, array)
+                boxes.append(self._window_box(dst, win, "lo" if d == E else "hi", False, dst))
+            if len(self._pulls) > 1024:
+                self._pulls.clear()
+            self._pulls[ck] = boxes
+        return boxes
 
     def open_peer_buffers(self, tables: list) -> None:
         """Install the peers' buffer handle tables. Mappings are opened lazily
@@ -169,6 +288,11 @@ class IpcPeerTransport(LocalPeerTransport):
                 for d in dirs:
                     nb = neighbour(self.store.decomp, info.rank, coords, d)
                     if nb is None or owners.get(nb, self.w) == self.w:
+                        continue
+                    if self._uses_windows(a):
+                        if (owners[nb], tuple(nb), ("win", a)) in self.peer_tables:
+                            self.peer_window(owners[nb], nb, a)
+                            peers.add(owners[nb])
                         continue
                     for arr in (a, ("twin", a)):
                         key = (owners[nb], tuple(nb), arr)
@@ -235,6 +359,10 @@ class IpcPeerTransport(LocalPeerTransport):
         r = self.seq
         self.seq += 1
         elem = ELEM[self.store.arrays[array].dtype]
+        if self._uses_windows(array):
+            exports = self._export_boxes(array, twin)
+            if exports:
+                self.dev.copy_boxes(exports, elem)
         self.dev.flag_write(self.flags + READY_OFF, r + 1, COMPUTE)
         if local_boxes:
             self.dev.copy_boxes(local_boxes, elem)
@@ -289,6 +417,8 @@ class IpcPeerTransport(LocalPeerTransport):
         self.close_arenas()
         for e in self.ready + self.pulled:
             e.close()
+        self.windows.clear()
+        self.hpool.release()
 
 
 class IpcGpuJob:

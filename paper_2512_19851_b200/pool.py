@@ -55,9 +55,10 @@ class _Arena:
 
 
 class DevicePool:
-    def __init__(self, dev, arena_min: int = ARENA_MIN):
+    def __init__(self, dev, arena_min: int = ARENA_MIN, grow: int = GROW):
         self.dev = dev
         self.arena_min = arena_min
+        self.grow = grow
         self.arenas: list = []
         self.live: dict = {}  # ptr -> (arena, offset, reserved bytes)
 
@@ -72,7 +73,7 @@ class DevicePool:
         else:
             # room for three more buffers of this size: a shrink that doubles the
             # tiles per worker then needs no cudaMalloc and no new peer mapping
-            arena = _Arena(self.dev, max(GROW * need, self.arena_min))
+            arena = _Arena(self.dev, max(self.grow * need, self.arena_min))
             self.arenas.append(arena)
             off = arena.take(need)
         ptr = arena.base + off

@@ -253,7 +253,8 @@ class GpuWorker:
             return
         self.job = self._new_job(decomp, owner_map_from_manifest(manifest))
         t1 = time.perf_counter()
-        depths = restore_tiles(self.job, manifest)
+        rst: dict = {}
+        depths = restore_tiles(self.job, manifest, rst)
         t2 = time.perf_counter()
         self.job.executor.depths = depths
         for a, info in self.job.store.arrays.items():
@@ -261,8 +262,8 @@ class GpuWorker:
             self.job.dtypes[a] = info.dtype
             self.job._next = max(self.job._next, a + 1)
         self.job.exchange_buffers()
-        log.info("restore: job %.1f ms, copies %.1f ms, peer maps %.1f ms", (t1 - t0) * 1e3,
-                 (t2 - t1) * 1e3, (time.perf_counter() - t2) * 1e3)
+        log.info("restore: job %.1f ms, tiles %.1f ms %s, peer maps %.1f ms", (t1 - t0) * 1e3,
+                 (t2 - t1) * 1e3, json.dumps(rst), (time.perf_counter() - t2) * 1e3)
         send_json(self.coord, REPLY_OK, {})
 
     def shutdown(self) -> None:
@@ -316,6 +317,9 @@ def worker_main(argv=None) -> int:
     ap.add_argument("--device", type=int, default=None)
     ap.add_argument("--standby", action="store_true")
     args = ap.parse_args(argv)
+    if os.environ.get("EST_WORKER_LOG"):  # stage splits of batches / migrate / restore on stderr
+        logging.basicConfig(level=logging.INFO, stream=sys.stderr,
+                            format="%(asctime)s %(name)s %(message)s")
     dev = None
     if args.standby:
         args.id, dev = standby(args.device or 0)

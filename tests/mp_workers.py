@@ -62,7 +62,11 @@ def host_logic_rank(rank, world, kind, odf, batch, chains=False):
            "tiles": sorted(job.store.tiles),
            "tb_launches": sum(1 for e in job.dev.log if e[0] == "launch" and e[2] == "est_tb"),
            "twins": len(job.store.twins),
-           "peer_twins": sum(1 for k in job.transport.peer_maps if isinstance(k[2], tuple)),
+           "peer_windows": len(job.transport.window_maps),
+           "peer_tile_maps": len(job.transport.peer_maps),
+           "exports": sum(1 for c in job.dev.copies if c[0] == "strip" and
+                          any(p <= c[2] < p + 2 * sig[3][0] * sig[1] * sig[5]
+                              for p, sig in job.transport.windows.values())),
            "flag_waits": sum(1 for e in job.dev.log if e[0] == "flag_wait")}
     job.close()
     return out

@@ -40,9 +40,11 @@ def test_rounds_and_handshake_across_processes(kind, world, odf, batch):
 @pytest.mark.parametrize("world,odf,batch", [(2, 1, 8), (2, 2, 20), (4, 1, 12)])
 def test_slab_chains_across_processes(world, odf, batch):
     """Temporal chains on z-slabs of a multi-process job: every rank runs the
-    chain kernel on its slabs, maps its neighbours' twin buffers, rounds are
-    sequenced identically everywhere and equal the reference EpochSimulator's
-    counts (the intermediate array's rounds are virtual)."""
+    chain kernel on its slabs, rounds are sequenced identically everywhere
+    and equal the reference EpochSimulator's counts (the intermediate array's
+    rounds are virtual). Halo planes travel through the owners' halo windows
+    (exported from home or twin, whichever holds the array): no rank maps a
+    neighbour's tile or twin buffer."""
     res = spawn_local_job(world, host_logic_rank, "heat3d", odf, batch, True, timeout=300)
     want = expected_rounds("heat3d", batch)
     for r in res:
@@ -50,7 +52,7 @@ def test_slab_chains_across_processes(world, odf, batch):
         assert r["tb_launches"] > 0 and r["twins"] == odf
         assert r["flag_waits"] > 0
     assert len({r["seq"] for r in res}) == 1
-    assert all(r["peer_twins"] > 0 for r in res)
+    assert all(r["peer_windows"] > 0 and r["peer_tile_maps"] == 0 and r["exports"] > 0 for r in res)
 
 
 @pytest.mark.parametrize("kind,world,shrink_to", [("heat3d", 4, 2), ("laplace", 4, 2), ("heat3d", 4, 1)])
