@@ -167,3 +167,52 @@ def single_tile_chain_rank(rank, world, kind):
                 "tiles": len(job.store.tiles)}
     finally:
         job.close()
+
+
+def checkpoint_rank(rank, world, address, manifest_path):
+    """A one-worker job fills a 3-D array, checkpoints into the daemon and
+    writes the manifest; returns the arrays' content hashes."""
+    import json
+
+    from paper_2512_19851_b200.daemon import DaemonClient
+    from paper_2512_19851_b200.elastic import build_manifest, checkpoint_tiles
+    from paper_2512_19851_b200.ipc import IpcGpuJob
+    from paper_2512_19851_b200.programs import DagProgram, heat3d_program
+
+    prog = DagProgram()
+    heat3d_program(prog, 48, 6, seed_fills=10)
+    job = IpcGpuJob(rank, world, device=0)
+    try:
+        for aid in sorted(prog.shapes):
+            job.create_array(prog.shapes[aid])
+        job.run(prog.dag)
+        hashes = {a: job.hash(a) for a in sorted(prog.shapes)}
+        c = DaemonClient(address)
+        try:
+            records, meta = checkpoint_tiles(job, c, rank)
+        finally:
+            c.close()
+        with open(manifest_path, "w") as fh:
+            json.dump(build_manifest(1, world, job.store.decomp, meta, records), fh)
+        return {"hashes": hashes, "records": len(records)}
+    finally:
+        job.close()
+
+
+def restore_rank(rank, world, manifest_path):
+    from paper_2512_19851_b200.elastic import (decomp_from_manifest, owner_map_from_manifest, read_manifest,
+                                               restore_tiles)
+    from paper_2512_19851_b200.ipc import IpcGpuJob
+
+    m = read_manifest(manifest_path)
+    job = IpcGpuJob(rank, world, device=0, decomp=decomp_from_manifest(m), owner_map=owner_map_from_manifest(m))
+    try:
+        stats = {}
+        depths = restore_tiles(job, m, stats)
+        job.executor.depths = depths
+        for a, info in job.store.arrays.items():
+            job.shapes[a] = info.shape
+        job.exchange_buffers()
+        return {"hashes": {a: job.hash(a) for a in sorted(job.store.arrays)}, "stats": stats}
+    finally:
+        job.close()
