@@ -306,7 +306,6 @@ class _Emitter:
         W0, W1, W1p, P1, NT, E = lay["w0"], lay["w1"], lay["w1p"], lay["p1"], lay["nt"], lay["elem"]
         m0, m1, BX = lay["m0"], lay["m1"], lay["bx"]
         rot = lay["cen"] is not None
-        tmap_p = rot
         PY, VT, T = self.py, self.VT, self.T
         NW = NT // 32
         H = RB + 2 * ry  # register window rows
@@ -349,15 +348,15 @@ class _Emitter:
         a(f"  if (warp == {NW}) {{")
         a("    if ((tid & 31) != 0) return;")
         a("    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tq) : \"memory\");")
-        if tmap_p:
+        if rot:
             a("    asm volatile(\"prefetch.tensormap [%0];\" :: \"l\"(&p.tp) : \"memory\");")
         a("    for (int s = 0; s < nst; ++s) {")
         a(f"      const int stg = s % {S0};")
         a(f"      if (s >= {S0}) mbar_wait(empty + stg, ((s / {S0}) - 1) & 1);")
-        a(f"      mbar_expect(full + stg, {RB * W0 * E * (2 if tmap_p else 1)});")
+        a(f"      mbar_expect(full + stg, {RB * W0 * E * (2 if rot else 1)});")
         a(f"      unsigned char* sb = smem + stg * {lay['stage']};")
         a(f"      tma_load3(sb, &p.tq, x0 + {self.xoff - m0}, ys - {2 * ry} + s * {RB}, 0, full + stg);")
-        if tmap_p:
+        if rot:
             a(f"      tma_load3(sb + {lay['qb']}, &p.tp, x0 + {self.xoff - m0}, ys - {3 * ry} + s * {RB}, 0, full + stg);")
         a("    }")
         a("    return;")
@@ -385,7 +384,7 @@ class _Emitter:
         a(f"{i2}mbar_wait(full + stg, ph);")
         a(f"{i2}const T* QS = reinterpret_cast<const T*>(smem + stg * {lay['stage']}) + {m0 - m1} + c * {V};")
         a(f"{i2}const T* QP = reinterpret_cast<const T*>(smem + prv * {lay['stage']}) + {m0 - m1} + c * {V};")
-        if tmap_p:
+        if rot:
             a(f"{i2}const T* PS = reinterpret_cast<const T*>(smem + stg * {lay['stage']} + {lay['qb']}) + {m0 - m1} + c * {V};")
 
         a(f"{i2}T* WB = ring1 + bk * {RB * W1p};  // ring bank of this stage's step-1 rows")
