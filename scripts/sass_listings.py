@@ -42,6 +42,14 @@ def hot_sources() -> dict:
     rs = stmt_sig(plan.statements[0], 2)
     g = resident.smem_geometry(1022, 1022, resident.slot_radius(rs)[0], 0, 148)
     out["c1_est_resident_smem"] = resident.smem_source(rs, 0, g)[0]
+    from paper_2512_19851_b200 import temporal2d
+    xoff, py, _pz = TileBuffer.pitches((16384, 16384), (1, 1), 0)
+    out["lap16k_est_tc"] = temporal2d.source(rs, 0, py=py, xoff=xoff)[0]
+    p = DagProgram()
+    wave2d_program(p, 64, 2, dtype=DTYPE_F32)
+    plan = compile_plan(p.dag.nodes[-1], p.dag.ast_table)
+    xoff, py, _pz = TileBuffer.pitches((16384, 16384), (2, 2), DTYPE_F32)
+    out["c3_est_tc_rotation_f32"] = temporal2d.source(stmt_sig(plan.statements[0], 2), DTYPE_F32, py=py, xoff=xoff)[0]
     return out
 
 
