@@ -227,10 +227,16 @@ def cpu_sample(w, iters: int = 2, planes: int = 34, threads: int = 0) -> dict:
         u = [prog.create_array(shape, DTYPE_F32) for _ in range(3)]
         prog.assign(u[2], (slice(2, -2), slice(2, -2)), wave2d_tree(u[0], u[1]))
         sample = f"{iters} wave steps over a {rows}x{n} row-slab of the {n}^2 grid"
-    else:
+    elif n <= 2048:
         shape = (n, n)
         laplace_program(prog, n, 1)
         sample = f"{iters} Jacobi iterations over the full {n}^2 grid"
+    else:
+        from paper_2512_19851_b200.programs import laplace_iteration_statements
+        shape = (max(planes * 16, 64), n)
+        u = [prog.create_array(shape) for _ in range(2)]
+        laplace_iteration_statements(prog, u[0], u[1], 1)
+        sample = f"{iters} Jacobi iterations over a {shape[0]}x{n} row-slab of the {n}^2 grid"
     node = prog.dag.nodes[-1]
     plan = compile_plan(node, prog.dag.ast_table).statements[0]
     dt = np.float32 if w["dtype"] == "f32" else np.float64
@@ -300,10 +306,15 @@ def reference_evaluator_sample(w, planes: int = 34, iters: int = 1) -> dict | No
             prog.assign(u[2], (slice(2, -2), slice(2, -2)), P.wave2d_tree(u[0], u[1]))
             sample = (f"{iters} wave step(s) over a {shape[0]}x{n} row-slab of the {n}^2 grid "
                       "(float64: the reference has no fp32 path)")
-        else:
+        elif n <= 2048:
             shape = (n, n)
             P.laplace_program(prog, n, 1)
             sample = f"{iters} Jacobi iteration(s) over the full {n}^2 grid"
+        else:  # the paper shape: a row-slab (a full 16384^2 pair per process would not fit host memory x 8)
+            shape = (max(planes * 16, 64), n)
+            u = [prog.create_array(shape) for _ in range(2)]
+            P.laplace_iteration_statements(prog, u[0], u[1], 1)
+            sample = f"{iters} Jacobi iteration(s) over a {shape[0]}x{n} row-slab of the {n}^2 grid"
     finally:
         for k, v in saved.items():
             setattr(P, k, v)
