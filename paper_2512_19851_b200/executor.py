@@ -460,7 +460,7 @@ class GpuExecutor:
                    and cand[j][0] == cand[j - 1][1] and cand[j][1] == cand[j - 1][0]):
                 j += 1
             sig = codegen.stmt_sig(plans[i].statements[0], c[4])
-            if (not multi and self.resident_smem and j - i >= 2 and resident.smem_eligible(sig, c[5], c[4])
+            if (n_tiles == 1 and self.resident_smem and j - i >= 2 and resident.smem_eligible(sig, c[5], c[4])
                     and self._rsm_geometry(c, sig) is not None):
                 sched[dag.nodes[i].node_id] = ("rsm", j - i)
                 for q in range(i + 1, j):
@@ -696,6 +696,8 @@ class GpuExecutor:
         shared memory, KM sweeps per pair of grid barriers (resident.py)."""
         ps = plan.statements[0]
         a, b = ps.inputs[0], ps.output
+        if not self.store.tiles:
+            return  # a worker without the (single) tile keeps the bookkeeping only
         tile = next(iter(self.store.tiles.values()))
         ba, bb = tile.buffers[a], tile.buffers[b]
         info = self.store.arrays[a]

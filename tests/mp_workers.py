@@ -134,11 +134,12 @@ def migrate_rank(rank, world, kind, shrink_to):
     return out
 
 
-def single_tile_chain_rank(rank, world, kind):
+def single_tile_chain_rank(rank, world, kind, rsm=False):
     """A single-tile 2-D job whose worker owns a transport (the GPU worker
     process, world 1 or a job whose other ranks own no tile): the rank-2
-    chain kernel (est_tc) runs there too. Returns the kernels launched by one
-    step and the arrays' final epochs."""
+    chain kernel (est_tc) runs there too, or with `rsm` the small-grid
+    shared-memory-resident run. Returns the kernels launched by one step and
+    the arrays' final epochs."""
     import paper_2512_19851_b200.ipc as ipc
     from fakedev import FakeDevice
     from paper_2512_19851_b200 import temporal2d
@@ -153,6 +154,7 @@ def single_tile_chain_rank(rank, world, kind):
     decomp = decompose((64, 64), 1, 1)   # one tile, owned by rank 0
     job = ipc.IpcGpuJob(rank, world, decomp=decomp, owner_map={c: 0 for c in decomp.all_coords()})
     try:
+        job.executor.resident_smem = rsm
         for a in sorted(prog.shapes):
             job.create_array(prog.shapes[a])
         job.run(prog.dag)

@@ -189,3 +189,14 @@ def test_chain_runs_in_worker_job_with_transport(world):
     assert len(owner) == 1 and owner[0]["names"].count("est_tc") == 4
     assert len({tuple(sorted(r["epochs"].items())) for r in res}) == 1
     assert all(not r["names"] for r in res if not r["tiles"])
+
+
+def test_resident_run_in_worker_job_with_transport():
+    """The same for a small grid: the whole 8-sweep run is one
+    shared-memory-resident launch in the worker's job (the reference-facing
+    seam path of C1)."""
+    from mp_workers import single_tile_chain_rank
+    from paper_2512_19851_b200.ipc import spawn_local_job
+
+    (res,) = spawn_local_job(1, single_tile_chain_rank, "laplace", True, timeout=300)
+    assert res["names"].count("est_resident_smem") == 1 and "est_tc" not in res["names"]
