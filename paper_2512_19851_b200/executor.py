@@ -182,7 +182,8 @@ class GpuExecutor:
         whose DAG and epoch / layout state repeat is replayed from a captured
         CUDA graph instead of being re-analysed and re-launched node by node;
         the epoch / round bookkeeping is applied exactly as a fresh run would."""
-        if key is None or not self.graphs or self.transport is not None or self.time_kernels:
+        if (key is None or not self.graphs or self.time_kernels
+                or (self.transport is not None and not getattr(self.transport, "graph_safe", lambda: False)())):
             return self._execute(dag, key)
         sig = (key, self._state_sig())
         ent = self._replay.get(sig)

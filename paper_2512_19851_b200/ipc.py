@@ -353,7 +353,17 @@ class IpcPeerTransport(LocalPeerTransport):
         return base
 
     # -- the round protocol on device flags ---------------------------------------
-    chains_ok = True  # peers map each other's twin buffers (buffer_table), so slabs chain
+    chains_ok = True  # halo planes go through the owners' windows (home or twin), so slabs chain
+
+    def graph_safe(self) -> bool:
+        """Batches may be captured into CUDA graphs and replayed when no peer
+        exists (a one-worker job: the GPU worker process behind a one-worker
+        coordinator). A replay re-writes this rank's READY / PULLED flags with
+        the captured values and does not advance `seq`; with peers those
+        words must grow monotonically, so multi-worker batches run
+        uncaptured. A later change of the worker count goes through a
+        restart (fresh transports) in the reference rescale."""
+        return self.job.world == 1
 
     def post(self, array: int, epoch: int, remote, local_boxes, twin: bool = False):
         r = self.seq

@@ -135,6 +135,7 @@ class FakeGraph:
     def launch(self, stream=0):
         self.launched += 1
         self.dev.launches += self.kernels
+        self.dev.log.append(("graph_launch", self.kernels, ""))
 
     def close(self):
         pass

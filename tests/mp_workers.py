@@ -218,3 +218,34 @@ def restore_rank(rank, world, manifest_path):
         return {"hashes": {a: job.hash(a) for a in sorted(job.store.arrays)}, "stats": stats}
     finally:
         job.close()
+
+
+def replay_rank(rank, world):
+    """Repeated 2-D Laplace batches (DAG bytes) on an IPC job with the device
+    double: replay counters, graph launches, final epochs and rounds."""
+    import paper_2512_19851_b200.ipc as ipc
+    from fakedev import FakeDevice
+    from paper_2512_19851_b200.programs import DagProgram, laplace_iteration_statements, laplace_program
+    from paper_2512_19851_b200.wire import encode_dag
+
+    ipc.Device = lambda device=0: FakeDevice(device, tag=f"r{rank}")
+    prog = DagProgram()
+    laplace_program(prog, 64, 0)
+    job = ipc.IpcGpuJob(rank, world)
+    try:
+        for a in sorted(prog.shapes):
+            job.create_array(prog.shapes[a])
+        job.run(prog.dag)
+        step = DagProgram()
+        for a in sorted(prog.shapes):
+            step.builder.declare_array(a, prog.shapes[a])
+        laplace_iteration_statements(step, 0, 1, 10)
+        blob = encode_dag(step.dag)
+        for _ in range(5):
+            job.run_bytes(blob)
+        return {"replays": job.executor.replays,
+                "graph_launches": sum(1 for e in job.dev.log if e[0] == "graph_launch"),
+                "epochs": {a: job.store.local_epoch(a) for a in sorted(prog.shapes)},
+                "rounds": dict(job.manager.rounds_started)}
+    finally:
+        job.close()

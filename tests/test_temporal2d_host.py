@@ -200,3 +200,17 @@ def test_resident_run_in_worker_job_with_transport():
 
     (res,) = spawn_local_job(1, single_tile_chain_rank, "laplace", True, timeout=300)
     assert res["names"].count("est_resident_smem") == 1 and "est_tc" not in res["names"]
+
+
+def test_one_worker_job_replays_graphs():
+    """A one-worker job behind the worker seam (a transport, no peers)
+    captures repeated batches into a CUDA graph and replays them, with the
+    same per-batch bookkeeping; a two-worker job never does."""
+    from mp_workers import replay_rank
+    from paper_2512_19851_b200.ipc import spawn_local_job
+
+    (one,) = spawn_local_job(1, replay_rank, timeout=300)
+    assert one["replays"] >= 2 and one["graph_launches"] >= 2
+    two = spawn_local_job(2, replay_rank, timeout=300)
+    assert all(r["replays"] == 0 for r in two)
+    assert one["epochs"] == two[0]["epochs"] and one["rounds"] == two[0]["rounds"]
