@@ -628,6 +628,8 @@ class IpcGpuJob:
             self.barrier()
         except Exception:
             pass
+        if self.executor is not None:
+            self.executor.drop_replays()  # captured graphs (one-worker jobs) and chain twins
         if self.transport is not None:
             self.transport.close()
         try:
