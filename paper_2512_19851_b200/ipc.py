@@ -188,7 +188,6 @@ class IpcPeerTransport(LocalPeerTransport):
                 nbytes = 2 * buf.depth[0] * buf.pz * buf.elem
                 self.windows[key] = (self.hpool.alloc(nbytes), self._window_sig(buf))
         self._exports.clear()
-        self._prepushed.clear()  # republished (possibly new) windows hold no pushed planes
 
     @staticmethod
     def _region(buf, win: int, region: str) -> int:
@@ -470,7 +469,6 @@ class IpcPeerTransport(LocalPeerTransport):
         self.job.sync()
         self.job.barrier()
         self.readers.clear()
-        self._prepushed.clear()  # windows may be re-made: the next round pushes in full
         self.close_peer_buffers()
 
     def after_realloc(self) -> None:
