@@ -33,10 +33,6 @@ from .device import COMPUTE
 from .errors import MalformedDag
 from .ir import validate_dag
 
-# chains on slabs store A's halo planes into the neighbours' receive windows
-# themselves (ipc halo windows); 0: the round after the chain pushes them
-FUSED_PUSH = os.environ.get("EST_FUSED_PUSH", "1") == "1"
-
 
 @dataclass
 class BatchStats:
@@ -318,10 +314,7 @@ class GpuExecutor:
                     self._round(a, target, refresh=True)
             t_node = time.perf_counter()
             plan = plans[node.node_id]
-            if self.transport is not None and not (chain is not None and chain[0] == "member"):
-                # a chain's lead covers every array the chain writes (a member
-                # launches nothing; its write already happened in the lead's
-                # kernel, which may also have pushed A's halo planes)
+            if self.transport is not None:
                 writes = set(node.writes)
                 if chain is not None and chain[0] in ("lead", "tc"):
                     writes |= set(plan.statements[0].inputs)  # the chain also writes A (or P)
@@ -766,24 +759,16 @@ class GpuExecutor:
                     self.dev.copy_boxes(grid, params)
                 else:
                     self.dev.launch(kern, grid, params, COMPUTE, self.transport is None, coop)
-        else:
-            self._recording = [] if ck is not None else None
-            try:
-                self._launch_tb_tiles(ps, a, b, ch, in_twin, last)
-            finally:
-                rec, self._recording = self._recording, None
-            if ck is not None and rec is not None:
-                self._launches[ck] = rec
+            self._in_twin[a] = not in_twin
+            return
+        self._recording = [] if ck is not None else None
+        try:
+            self._launch_tb_tiles(ps, a, b, ch, in_twin, last)
+        finally:
+            rec, self._recording = self._recording, None
+        if ck is not None and rec is not None:
+            self._launches[ck] = rec
         self._in_twin[a] = not in_twin
-        if self._pushes_fused(a):
-            self.transport.mark_pushed(a)  # the kernel stored A's halo planes into the peers' windows
-
-    def _pushes_fused(self, a: int) -> bool:
-        """Chains on slabs with remote neighbours store A's boundary planes
-        straight into the neighbours' receive windows (ipc halo windows)."""
-        tr = self.transport
-        return (tr is not None and FUSED_PUSH and hasattr(tr, "push_targets")
-                and any(tr.push_targets(c, a, t.buffers[a]) for c, t in self.store.tiles.items()))
 
     def _launch_tb_tiles(self, ps, a, b, ch, in_twin, last) -> None:
         info = self.store.arrays[a]
@@ -813,16 +798,6 @@ class GpuExecutor:
                 if self._recording is not None:
                     self._recording.append((None, boxes, home.elem, False))
             src_buf, dst_buf = (twin, home) if in_twin else (home, twin)
-            push = (self.transport.push_targets(coords, a, home)
-                    if FUSED_PUSH and hasattr(self.transport, "push_targets") else None)
-            if push is not None and ch == 0:
-                # the kernel stores only S's points; a full push of A's
-                # boundary planes first puts the rest (constant during the run)
-                # into the neighbours' windows
-                boxes = self.transport.tile_push_boxes(coords, a, home)
-                self.dev.copy_boxes(boxes, home.elem)
-                if self._recording is not None:
-                    self._recording.append((None, boxes, home.elem, False))
             src, name, block, smem, lay = temporal.source(sig, info.dtype, self.tb_cfg,
                                                           py=home.py, pz=home.pz, xoff=home.xoff)
             kern = self.dev.kernel(src, name, block, smem)
@@ -830,8 +805,7 @@ class GpuExecutor:
             tm = self._tmap(src_buf, (lay["w0"], lay["h0"], 1), self.tb_cfg.l2promo)
             org = home.xoff * home.elem
             params = temporal.pack_params(tm, src_buf.ptr + org, bbuf.ptr + org, dst_buf.ptr + org,
-                                          home, s_lo, s_hi, geo, write_b=last or not temporal.SKIP_MID_B, cz=cz,
-                                          push=push)
+                                          home, s_lo, s_hi, geo, write_b=last or not temporal.SKIP_MID_B, cz=cz)
             self._launch(kern, (geo["blocks"], 1, 1), params, tag=("tb", K))
 
     # -- node -> kernel launch ----------------------------------------------

@@ -103,9 +103,7 @@ class IpcPeerTransport(LocalPeerTransport):
         self.hpool = DevicePool(self.dev, HALO_ARENA, grow=2)
         self.flags = self.hpool.alloc(256)  # [READY_OFF] ready, [PULLED_OFF] pulled; zeroed
         self.windows: dict = {}  # (coords, array) -> (ptr, signature): the slab's boundary planes
-        self.window_maps: set = set()  # peers' windows this rank has pushed into (introspection)
-        self._prepushed: set = set()   # arrays whose next round was pushed by a chain kernel
-        self.fused_rounds = 0           # rounds whose halo planes a chain kernel pushed (introspection)
+        self.window_maps: set = set()  # peers' windows this rank has pulled from (introspection)
         self._exports: dict = {}
         self.ready = [self.dev.event() for _ in range(RING)]   # intra-process: copy lane after compute
         self.pulled = [self.dev.event() for _ in range(RING)]  # intra-process: compute after copy lane
@@ -200,73 +198,34 @@ class IpcPeerTransport(LocalPeerTransport):
     def _push_boxes(self, array: int, twin: bool) -> list:
         """Owner side of a round: this rank's boundary planes facing remote
         neighbours -> those neighbours' receive windows (peer memory)."""
+        from ._lib import EstBox
+        from .exchange import E, W, neighbour
+
         ck = (array, self.store.version, self.peer_version, id(self.job.owner_map), twin)
         boxes = self._exports.get(ck)
         if boxes is None:
             boxes = []
+            owners = self.job.owner_map or {}
+            info = self.store.arrays[array]
             for coords in sorted(self.store.tiles):
                 if (tuple(coords), array) not in self.windows:
                     continue
                 buf = self.store.twins[(coords, array)] if twin else self.store.tiles[coords].buffers[array]
-                boxes += self.tile_push_boxes(coords, array, buf)
+                pd = buf.depth[0]
+                ez, ey, ex = buf.ext
+                for d in (W, E):
+                    nb = neighbour(self.store.decomp, info.rank, coords, d)
+                    if nb is None or owners.get(nb, self.w) == self.w:
+                        continue
+                    win = self.peer_window(owners[nb], nb, array)
+                    # our low planes are the W neighbour's high ghost planes, and vice versa
+                    src = buf.interior_addr((0 if d == W else ez - pd, 0, 0))
+                    dst = self._region(buf, win, "hi" if d == W else "lo")
+                    boxes.append(EstBox(src, dst, buf.py, buf.pz, buf.py, buf.pz, ex, ey, pd))
             if len(self._exports) > 256:
                 self._exports.clear()
             self._exports[ck] = boxes
         return boxes
-
-    def push_targets(self, coords, array: int, buf):
-        """Fused halo push of a chain kernel writing `array` of tile `coords`
-        (layout `buf`): ((pw, pw0, pw1), (pe, pe0, pe1)) = the W / E remote
-        neighbours' receive windows as padded-box origins of this tile's
-        padded planes [pw0, pw1) / [pe0, pe1) (0: no push on that side), or
-        None when the tile has no remote neighbour."""
-        from .exchange import E, W, neighbour
-
-        if not self._uses_windows(array) or (tuple(coords), array) not in self.windows:
-            return None
-        owners = self.job.owner_map or {}
-        info = self.store.arrays[array]
-        pd, (dz, dy, dx) = buf.depth[0], buf.depth
-        ez = buf.ext[0]
-        out = []
-        for d in (W, E):
-            nb = neighbour(self.store.decomp, info.rank, coords, d)
-            if nb is None or owners.get(nb, self.w) == self.w:
-                out.append((0, 0, 0))
-                continue
-            z0 = dz if d == W else dz + ez - pd
-            region = self._region(buf, self.peer_window(owners[nb], nb, array), "hi" if d == W else "lo")
-            # padded (z0, dy, dx) of this tile lands on the region's first interior point
-            origin = region - (z0 * buf.pz + dy * buf.py + dx) * buf.elem
-            out.append((origin, z0, z0 + pd))
-        return tuple(out) if any(t[0] for t in out) else None
-
-    def tile_push_boxes(self, coords, array: int, buf) -> list:
-        """The full push of one tile's boundary planes (from `buf`) into its
-        remote neighbours' receive windows."""
-        from ._lib import EstBox
-        from .exchange import E, W, neighbour
-
-        owners = self.job.owner_map or {}
-        info = self.store.arrays[array]
-        pd = buf.depth[0]
-        ez, ey, ex = buf.ext
-        boxes = []
-        for d in (W, E):
-            nb = neighbour(self.store.decomp, info.rank, coords, d)
-            if nb is None or owners.get(nb, self.w) == self.w:
-                continue
-            win = self.peer_window(owners[nb], nb, array)
-            # our low planes are the W neighbour's high ghost planes, and vice versa
-            src = buf.interior_addr((0 if d == W else ez - pd, 0, 0))
-            dst = self._region(buf, win, "hi" if d == W else "lo")
-            boxes.append(EstBox(src, dst, buf.py, buf.pz, buf.py, buf.pz, ex, ey, pd))
-        return boxes
-
-    def mark_pushed(self, array: int) -> None:
-        """The array's boundary planes already sit in the neighbours' windows
-        (a chain kernel stored them there): its next round only signals."""
-        self._prepushed.add(array)
 
     def peer_window(self, owner: int, coords, array: int) -> int:
         """Mapped address of `owner`'s receive window of (coords, array)."""
@@ -421,13 +380,10 @@ class IpcPeerTransport(LocalPeerTransport):
         r = self.seq
         self.seq += 1
         elem = ELEM[self.store.arrays[array].dtype]
-        if self._uses_windows(array) and array not in self._prepushed:
+        if self._uses_windows(array):
             pushes = self._push_boxes(array, twin)
             if pushes:
                 self.dev.copy_boxes(pushes, elem)
-        elif array in self._prepushed:
-            self.fused_rounds += 1
-        self._prepushed.discard(array)
         self.dev.flag_write(self.flags + READY_OFF, r + 1, COMPUTE)
         if local_boxes:
             self.dev.copy_boxes(local_boxes, elem)
@@ -457,7 +413,6 @@ class IpcPeerTransport(LocalPeerTransport):
         self.pulled[r % RING].wait(COMPUTE)
 
     def before_write(self, array: int) -> None:
-        self._prepushed.discard(array)  # the windows will hold stale planes after this write
         ent = self.readers.pop(array, None)
         if ent is None:
             return

@@ -274,10 +274,7 @@ class _Emitter:
         a("struct __align__(64) Tmap { unsigned long long w[16]; };")
         a("struct __align__(64) Params { Tmap tm;")
         a("  unsigned long long src, bhome, adst;  // padded-box origins: A now, B (in place), A next")
-        a("  unsigned long long pw, pe;  // fused halo push: the W / E neighbours' receive windows, as padded-box")
-        a("                              // origins of the planes [pw0, pw1) / [pe0, pe1) (0: no remote neighbour)")
-        a("  int npz, npy, npx, sz0, sz1, sy0, sy1, sx0, sx1, xt0, nbx, nby, zc, nzc, wb, cz0, cz1,")
-        a("      pw0, pw1, pe0, pe1; };")
+        a("  int npz, npy, npx, sz0, sz1, sy0, sy1, sx0, sx1, xt0, nbx, nby, zc, nzc, wb, cz0, cz1; };")
         a(_PTX_HELPERS)
         a("__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {")
         a("  asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(smem_u32(b)) : \"memory\"); }")
@@ -386,9 +383,6 @@ class _Emitter:
         VT = self.VT
         a = self.a
         a(f"{ind}T* ap = adst + (long long)zs * {PZ} + gb;  // step-K plane (A next)")
-        a(f"{ind}const bool pwn = p.pw != 0ull, pen = p.pe != 0ull;  // fused halo push targets")
-        a(f"{ind}T* pwp = reinterpret_cast<T*>(p.pw) + gb;")
-        a(f"{ind}T* pep = reinterpret_cast<T*>(p.pe) + gb;")
         a(f"{ind}T* bp = bmem + (long long)(zs - {rz}) * {PZ} + gb;  // step-(K-1) plane (B)")
         a(f"{ind}const T* ring0 = reinterpret_cast<const T*>(smem);")
         a(f"{ind}int tr = 0;  // t mod R (intermediate ring slots)")
@@ -453,7 +447,6 @@ class _Emitter:
                     a(f"{i4}if (zs{j}) {{")
                 else:
                     a(f"{i4}{{")
-                    a(f"{i4}const long long uK = zs - {2 * K * rz} + t;  // plane of the step-K output")
                 i5 = i4 + "  "
                 if not cfg.hoist:
                     ptr, need, pitch = loads[j]
@@ -476,10 +469,6 @@ class _Emitter:
                     targets = []
                     if final:
                         targets.append(("ap", f"in{K}_{r}"))
-                        # fused halo push: A's final boundary planes also go
-                        # straight into the neighbours' receive windows
-                        targets.append((f"(pwp + {PZ} * uK)", f"pwn && uK >= p.pw0 && uK < p.pw1 && in{K}_{r}"))
-                        targets.append((f"(pep + {PZ} * uK)", f"pen && uK >= p.pe0 && uK < p.pe1 && in{K}_{r}"))
                     if j == K - 1:
                         targets.append(("bp", f"wb && in{K}_{r} && u{j} >= zs && u{j} < zs + nzl"))
                     for ptr, cond in targets:
@@ -560,7 +549,7 @@ def item_geometry(s_lo, s_hi, sm_count: int, lay: dict, xoff: int = 0) -> dict:
 
 
 def pack_params(tmap: bytes, src: int, bhome: int, adst: int, buf, s_lo, s_hi, geo: dict,
-                write_b: bool = True, cz=None, push=None) -> bytes:
+                write_b: bool = True, cz=None) -> bytes:
     """Params block (layout mirrored in `source`). Pointers are padded-box
     origins (buffer base + xoff elements). `write_b` False skips B's stores:
     inside a run only the last chain's B survives (the next chain overwrites
@@ -569,21 +558,15 @@ def pack_params(tmap: bytes, src: int, bhome: int, adst: int, buf, s_lo, s_hi, g
     the statement (the global output slice within reach of this tile): on a
     slab of a multi-tile job it extends past the tile's own output planes
     into the ghost planes that belong to the neighbour's output (default:
-    the tile's own output planes [s_lo[0], s_hi[0])).
-    `push` = ((pw, pw0, pw1), (pe, pe0, pe1)): the fused halo push of a slab
-    with remote neighbours (ipc.IpcPeerTransport.push_targets): A's final
-    values on the padded planes [pw0, pw1) / [pe0, pe1) are also stored at
-    the W / E neighbour's receive window, given as a padded-box origin (0:
-    no push on that side)."""
+    the tile's own output planes [s_lo[0], s_hi[0]))."""
     assert len(tmap) == 128
     npz, npy, npx = buf.nz, buf.pz // buf.py, buf.ext[2] + 2 * buf.depth[2]
     cz0, cz1 = cz if cz is not None else (s_lo[0], s_hi[0])
-    (pw, pw0, pw1), (pe, pe0, pe1) = push or ((0, 0, 0), (0, 0, 0))
     out = bytearray(tmap)
-    out += struct.pack("<QQQQQ", src, bhome, adst, pw, pe)
-    out += struct.pack("<21i", npz, npy, npx, s_lo[0], s_hi[0], s_lo[1], s_hi[1],
+    out += struct.pack("<QQQ", src, bhome, adst)
+    out += struct.pack("<17i", npz, npy, npx, s_lo[0], s_hi[0], s_lo[1], s_hi[1],
                        s_lo[2], s_hi[2], geo["xt0"], geo["nbx"], geo["nby"], geo["zc"], geo["nzc"], int(write_b),
-                       cz0, cz1, pw0, pw1, pe0, pe1)
+                       cz0, cz1)
     return bytes(out) + b"\0" * ((-len(out)) % 64)
 
 

@@ -3,7 +3,6 @@
 from __future__ import annotations
 
 import os
-import struct
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -64,9 +63,6 @@ def host_logic_rank(rank, world, kind, odf, batch, chains=False):
            "tb_launches": sum(1 for e in job.dev.log if e[0] == "launch" and e[2] == "est_tb"),
            "twins": len(job.store.twins),
            "peer_windows": len(job.transport.window_maps),
-           "fused_rounds": job.transport.fused_rounds,
-           "fused_launches": sum(1 for e, prm in zip([e for e in job.dev.log if e[0] == "launch"], job.dev.params)
-                                 if e[2] == "est_tb" and any(struct.unpack_from("<QQ", prm, 128 + 24))),
            "peer_tile_maps": len(job.transport.peer_maps),
            # receiver side of a push round: own receive window -> own ghost planes
            "exports": sum(1 for c in job.dev.copies if c[0] == "strip" and

@@ -55,9 +55,6 @@ def test_slab_chains_across_processes(world, odf, batch):
         assert r["flag_waits"] > 0
     assert len({r["seq"] for r in res}) == 1
     assert all(r["peer_windows"] > 0 and r["peer_tile_maps"] == 0 and r["exports"] > 0 for r in res)
-    # the chain kernels store A's halo planes into the neighbours' windows
-    # themselves; the rounds right after a chain only signal
-    assert all(r["fused_launches"] > 0 and r["fused_rounds"] > 0 for r in res)
 
 
 @pytest.mark.parametrize("kind,world,shrink_to", [("heat3d", 4, 2), ("laplace", 4, 2), ("heat3d", 4, 1)])

@@ -313,8 +313,7 @@ def test_b_written_only_by_the_last_chain_of_a_run():
     ex.execute_batch(step.dag)
     tb = [p for e, p in zip(dev.log, dev.params) if e[2] == "est_tb"]
     assert len(tb) == 4
-    # Params: tensor map (128 B), 5 pointers (src, bhome, adst, pw, pe), then ints; wb is the 15th int
-    assert [struct.unpack_from("<i", p, 128 + 40 + 14 * 4)[0] for p in tb] == [0, 0, 0, 1]
+    assert [struct.unpack_from("<i", p, 128 + 24 + 14 * 4)[0] for p in tb] == [0, 0, 0, 1]
 
 
 def test_self_dependent_statement_is_rejected_before_any_launch():
