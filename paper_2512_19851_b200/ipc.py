@@ -150,19 +150,14 @@ class IpcPeerTransport(LocalPeerTransport):
         return out
 
     # -- halo windows (rank-3 slabs) -----------------------------------------------
-    # Every owned (slab, array) has a small RECEIVE window in the halo arena:
-    # region "lo" takes the W neighbour's last pd interior planes (our low
-    # ghost planes), region "hi" the E neighbour's first pd (our high ghost
-    # planes); pd = the array's physical z ghost depth. A round is a push:
-    # the owner's compute stream copies its boundary planes (from home or the
-    # temporal chain's twin, whichever holds the array) straight into the
-    # neighbours' windows over peer memory (NVLink stores on a multi-GPU box)
-    # and writes READY; the receiver waits READY and copies its own window
-    # into its ghost planes (local), then writes PULLED; the owner's next
-    # write into that window waits PULLED (`before_write`). Peers map only
-    # each other's halo arenas (a few MiB), never the GiB-sized tile arenas
-    # (~50-65 ms per GiB mapped: 0.6-1.5 s of every restore before,
-    # profiles/r2_c5_halo_windows_probe*.json). Cost: 2*pd planes per round
+    # A slab's neighbours read only its pd boundary planes on each side (pd =
+    # the array's physical z ghost depth). Before READY the owner copies those
+    # planes (from whichever buffer holds the array: home, or the temporal
+    # chain's twin mid-run) into a small window [lo: pd planes | hi: pd
+    # planes] in the halo arena, and the neighbours pull from the window. A
+    # restarted or re-mapped worker then maps a few MiB per neighbour instead
+    # of the neighbour's whole tile arena (~65 ms per GiB mapped,
+    # profiles/r2_c5_stage_split.md). The copy costs 2*pd planes per round
     # (C4 on 8 GPUs: 32 MiB, ~10 us, against ~0.5 ms of chain compute).
 
     @staticmethod
@@ -187,21 +182,30 @@ class IpcPeerTransport(LocalPeerTransport):
                 self.windows[key] = (self.hpool.alloc(nbytes), self._window_sig(buf))
         self._exports.clear()
 
-    @staticmethod
-    def _region(buf, win: int, region: str) -> int:
-        """Address of interior (y, x) = (0, 0) of the first plane of a window
-        region ("lo" / "hi"); windows share the tile buffers' pitches."""
-        pd = buf.depth[0]
-        inplane = (buf.xoff + buf.depth[1] * buf.py + buf.depth[2]) * buf.elem
-        return win + (0 if region == "lo" else pd * buf.pz * buf.elem) + inplane
-
-    def _push_boxes(self, array: int, twin: bool) -> list:
-        """Owner side of a round: this rank's boundary planes facing remote
-        neighbours -> those neighbours' receive windows (peer memory)."""
+    def _window_box(self, buf, win: int, side: str, export: bool, dst_buf=None):
+        """Copy descriptor between a slab's boundary planes and a window
+        region: `side` "lo" = the first pd interior planes, "hi" = the last
+        pd. export: slab -> own window; else window (a peer's, mapped at
+        `win`) -> the ghost planes of `dst_buf` on the side facing it."""
         from ._lib import EstBox
+
+        pd = buf.depth[0]
+        ez, ey, ex = buf.ext
+        inplane = (buf.xoff + buf.depth[1] * buf.py + buf.depth[2]) * buf.elem
+        region = win + (0 if side == "lo" else pd * buf.pz * buf.elem) + inplane
+        if export:
+            src = buf.interior_addr((0 if side == "lo" else ez - pd, 0, 0))
+            return EstBox(src, region, buf.py, buf.pz, buf.py, buf.pz, ex, ey, pd)
+        # the peer's lo planes fill our high ghost planes (it is our E
+        # neighbour), its hi planes our low ghost planes
+        gz = pd + ez if side == "lo" else 0
+        return EstBox(region, dst_buf.addr(gz, dst_buf.depth[1], dst_buf.depth[2]), buf.py, buf.pz,
+                      dst_buf.py, dst_buf.pz, ex, ey, pd)
+
+    def _export_boxes(self, array: int, twin: bool) -> list:
         from .exchange import E, W, neighbour
 
-        ck = (array, self.store.version, self.peer_version, id(self.job.owner_map), twin)
+        ck = (array, self.store.version, id(self.job.owner_map), twin)
         boxes = self._exports.get(ck)
         if boxes is None:
             boxes = []
@@ -211,24 +215,18 @@ class IpcPeerTransport(LocalPeerTransport):
                 if (tuple(coords), array) not in self.windows:
                     continue
                 buf = self.store.twins[(coords, array)] if twin else self.store.tiles[coords].buffers[array]
-                pd = buf.depth[0]
-                ez, ey, ex = buf.ext
-                for d in (W, E):
+                win = self.windows[(tuple(coords), array)][0]
+                for d, side in ((W, "lo"), (E, "hi")):
                     nb = neighbour(self.store.decomp, info.rank, coords, d)
-                    if nb is None or owners.get(nb, self.w) == self.w:
-                        continue
-                    win = self.peer_window(owners[nb], nb, array)
-                    # our low planes are the W neighbour's high ghost planes, and vice versa
-                    src = buf.interior_addr((0 if d == W else ez - pd, 0, 0))
-                    dst = self._region(buf, win, "hi" if d == W else "lo")
-                    boxes.append(EstBox(src, dst, buf.py, buf.pz, buf.py, buf.pz, ex, ey, pd))
+                    if nb is not None and owners.get(nb, self.w) != self.w:
+                        boxes.append(self._window_box(buf, win, side, True))
             if len(self._exports) > 256:
                 self._exports.clear()
             self._exports[ck] = boxes
         return boxes
 
     def peer_window(self, owner: int, coords, array: int) -> int:
-        """Mapped address of `owner`'s receive window of (coords, array)."""
+        """Mapped address of `owner`'s halo window of (coords, array)."""
         aserial, handle, off = self.peer_tables[(owner, tuple(coords), ("win", array))][:3]
         self.window_maps.add((owner, tuple(coords), array))
         base = self.arena_maps.get((owner, aserial))
@@ -240,27 +238,18 @@ class IpcPeerTransport(LocalPeerTransport):
         return WINDOWS and self.store.arrays[array].rank == 3
 
     def _pull_boxes(self, array: int, remote, twin: bool = False) -> list:
-        """Receiver side: rank-3 slabs copy their own receive windows (filled
-        by the neighbours' pushes) into their ghost planes; other ranks pull
-        the strips out of the neighbours' buffers."""
         if not self._uses_windows(array):
             return super()._pull_boxes(array, remote, twin)
-        from ._lib import EstBox
         from .exchange import E
 
         ck = (array, self.store.version, self.peer_version, id(remote), twin, "win")
         boxes = self._pulls.get(ck)
         if boxes is None:
             boxes = []
-            for coords, d, _nb, _owner in remote:
+            for coords, d, nb, owner in remote:
                 dst = self.store.twins[(coords, array)] if twin else self.store.tiles[coords].buffers[array]
-                win = self.windows[(tuple(coords), array)][0]
-                pd = dst.depth[0]
-                ez, ey, ex = dst.ext
-                src = self._region(dst, win, "hi" if d == E else "lo")
-                gz = pd + ez if d == E else 0
-                boxes.append(EstBox(src, dst.addr(gz, dst.depth[1], dst.depth[2]), dst.py, dst.pz,
-                                    dst.py, dst.pz, ex, ey, pd))
+                win = self.peer_window(owner, nb, array)
+                boxes.append(self._window_box(dst, win, "lo" if d == E else "hi", False, dst))
             if len(self._pulls) > 1024:
                 self._pulls.clear()
             self._pulls[ck] = boxes
@@ -381,9 +370,9 @@ class IpcPeerTransport(LocalPeerTransport):
         self.seq += 1
         elem = ELEM[self.store.arrays[array].dtype]
         if self._uses_windows(array):
-            pushes = self._push_boxes(array, twin)
-            if pushes:
-                self.dev.copy_boxes(pushes, elem)
+            exports = self._export_boxes(array, twin)
+            if exports:
+                self.dev.copy_boxes(exports, elem)
         self.dev.flag_write(self.flags + READY_OFF, r + 1, COMPUTE)
         if local_boxes:
             self.dev.copy_boxes(local_boxes, elem)

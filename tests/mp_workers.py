@@ -64,9 +64,8 @@ def host_logic_rank(rank, world, kind, odf, batch, chains=False):
            "twins": len(job.store.twins),
            "peer_windows": len(job.transport.window_maps),
            "peer_tile_maps": len(job.transport.peer_maps),
-           # receiver side of a push round: own receive window -> own ghost planes
            "exports": sum(1 for c in job.dev.copies if c[0] == "strip" and
-                          any(p <= c[1] < p + 2 * sig[3][0] * sig[1] * sig[5]
+                          any(p <= c[2] < p + 2 * sig[3][0] * sig[1] * sig[5]
                               for p, sig in job.transport.windows.values())),
            "flag_waits": sum(1 for e in job.dev.log if e[0] == "flag_wait")}
     job.close()

@@ -42,11 +42,9 @@ def test_slab_chains_across_processes(world, odf, batch):
     """Temporal chains on z-slabs of a multi-process job: every rank runs the
     chain kernel on its slabs, rounds are sequenced identically everywhere
     and equal the reference EpochSimulator's counts (the intermediate array's
-    rounds are virtual). Halo planes travel through halo windows: the owner
-    pushes its boundary planes (from home or twin, whichever holds the
-    array) into the neighbours' receive windows, the receiver copies its
-    window into its ghost planes; no rank maps a neighbour's tile or twin
-    buffer."""
+    rounds are virtual). Halo planes travel through the owners' halo windows
+    (exported from home or twin, whichever holds the array): no rank maps a
+    neighbour's tile or twin buffer."""
     res = spawn_local_job(world, host_logic_rank, "heat3d", odf, batch, True, timeout=300)
     want = expected_rounds("heat3d", batch)
     for r in res:
