@@ -66,7 +66,6 @@ class TcCfg:
     min_items: int = 2048
     l2promo: int = 2
     vec: int = 0         # bytes per thread vector (0: auto, 8 = fp32 pairs for rotations, else 16)
-    ring: int = 0        # step-1 row ring: 0 = three banks of RB rows, 1 = circular 2*RB + ry rows (less smem)
 
 
 def _env_cfg() -> TcCfg:
@@ -75,7 +74,7 @@ def _env_cfg() -> TcCfg:
     return TcCfg(bx=int(e("EST_TC_BX", d.bx)), rb=int(e("EST_TC_RB", d.rb)),
                  prefetch=int(e("EST_TC_PREFETCH", d.prefetch)), ychunk=int(e("EST_TC_YCHUNK", d.ychunk)),
                  min_items=int(e("EST_TC_MIN_ITEMS", d.min_items)), l2promo=int(e("EST_TC_L2PROMO", d.l2promo)),
-                 vec=int(e("EST_TC_VEC", d.vec)), ring=int(e("EST_TC_RING", d.ring)))
+                 vec=int(e("EST_TC_VEC", d.vec)))
 
 
 DEFAULT = _env_cfg()
@@ -144,10 +143,7 @@ def layout(st: StmtSig, dtype: int, cfg: TcCfg) -> dict:
     # have the same inner extent, a multiple of 32 bytes
     pb = _round(RB * W0 * elem, 128) if cen is not None else 0
     stage = qb + pb
-    # step-1 rows: three banks of RB (this stage, the previous, the next) or
-    # a circular ring of 2*RB + ry rows (the rows step 2 of this stage and
-    # step 1 of the next one touch at once)
-    C1 = 3 * RB if not cfg.ring else 2 * RB + ry
+    C1 = 3 * RB  # three banks of RB step-1 rows (this stage, the previous, the next)
     W1p = W1 + 2 * V
     ring1 = S0 * stage
     data = _round(ring1 + C1 * W1p * elem, 8)
@@ -218,15 +214,6 @@ class _Emitter:
             for c in sorted(comps):
                 self.a(f"{ind}const {self.T} n{step}{side}{i}_{c} = nv{step}{side}{i}.{'xyzw'[c]};")
 
-    def _ring_row(self, k: int) -> str:
-        """Pointer expression of the step-1 ring row of iteration tb + k
-        (k in [-ry, RB)) for this thread's column."""
-        lay = self.lay
-        RB, W1p, C1 = lay["rb"], lay["w1p"], lay["c1"]
-        if not lay["cfg"].ring:
-            return f"(WB + {k * W1p})" if k >= 0 else f"(WP + {(RB + k) * W1p})"
-        return f"(ring1 + ((r1b + {k + C1}) % {C1}) * {W1p})"
-
     def emit_stage(self, ind: str, fast: bool) -> None:
         """One stage: step 1 for RB rows, the named barrier, step 2 for RB rows.
         The fast variant (interior stages of items inside S in x) has no row
@@ -257,7 +244,7 @@ class _Emitter:
                 self._nbr_loads(i3, 1, i, need, base)
                 for v, (lines, res) in enumerate(bodies):
                     a(f"{i3}{{ " + " ".join(lines) + f" {out[v]} = {res}; }}")
-                a(f"{i3}*reinterpret_cast<{VT}*>({self._ring_row(i)}) = {vec};")
+                a(f"{i3}*reinterpret_cast<{VT}*>(WB + {i * W1p}) = {vec};")
                 a(f"{i3}if (p.wb && own) *reinterpret_cast<{VT}*>(x1m + r1 + {i * PY}) = {vec};")
                 a(f"{ind}}}")
                 continue
@@ -279,7 +266,7 @@ class _Emitter:
             for v in range(V):
                 a(f"{i5}{out[v]} = (yp && xp{v}) ? x1m[r1 + {i * PY + v}] : (T)0;")
             a(f"{i4}}}")
-            a(f"{i4}*reinterpret_cast<{VT}*>({self._ring_row(i)}) = {vec};")
+            a(f"{i4}*reinterpret_cast<{VT}*>(WB + {i * W1p}) = {vec};")
             a(f"{i4}if (p.wb && own && u1 >= ys && u1 < ys + nyl) {{")
             a(f"{i5}T* dst = x1m + r1 + {i * PY};")
             a(f"{i5}if (xin) *reinterpret_cast<{VT}*>(dst) = {vec};")
@@ -294,7 +281,7 @@ class _Emitter:
             i3 = ind + "  "
             cond = "" if fast else f"if (tb + {i} >= {4 * ry} && tb + {i} < n0) "
             a(f"{ind}{cond}{{  // step 2, unroll {i}: row t - {2 * ry}")
-            src = self._ring_row(i - ry)
+            src = f"(WB + {(i - ry) * W1p})" if i >= ry else f"(WP + {(RB + i - ry) * W1p})"
             a(f"{i3}const T* R = {src};")
             need = {}
             bodies = [self._expr(2, i, v, need) for v in range(V)]
@@ -390,7 +377,6 @@ class _Emitter:
             a(f"  T {', '.join(f'q{k}_{v} = 0' for v in range(V))};")
             a(f"  T {', '.join(f'x{k}_{v} = 0' for v in range(V))};")
         a("  int stg = 0, ph = 0, prv = 0, bk = 0, bp = 2;  // stage slot / phase, previous slot, ring banks")
-        a("  int r1b = 0;  // circular ring: slot of this stage's first step-1 row")
         a(f"  const bool xfast = (x0 - {m1} >= p.sx0) && (x0 + {BX + m1} <= p.sx1);  // frame inside S in x")
         a("  for (int s = 0; s < nst; ++s) {")
         i2 = "    "
@@ -416,8 +402,6 @@ class _Emitter:
         a(f"{i2}prv = stg;")
         a(f"{i2}if (++stg == {S0}) {{ stg = 0; ph ^= 1; }}")
         a(f"{i2}bp = bk; if (++bk == 3) bk = 0;")
-        if cfg.ring:
-            a(f"{i2}r1b += {RB}; if (r1b >= {C1}) r1b -= {C1};")
         a("  }")
         a("}")
         return "\n".join(self.L) + "\n"
