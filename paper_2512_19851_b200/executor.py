@@ -314,6 +314,11 @@ class GpuExecutor:
                     self._round(a, target, refresh=True)
             t_node = time.perf_counter()
             plan = plans[node.node_id]
+            if chain is not None and self.exchanges.pending:
+                # a chain also overwrites its input A: the round of A it reads
+                # must be complete on this side (so `readers` names the peers
+                # that read from us in it) before before_write waits on them
+                self.exchanges.finish_pending()
             if self.transport is not None:
                 writes = set(node.writes)
                 if chain is not None and chain[0] in ("lead", "tc"):
@@ -326,8 +331,6 @@ class GpuExecutor:
                 # kernel; members only keep the per-node bookkeeping (the
                 # halo rounds inside a chain are virtual: step 1 computes the
                 # intermediate array's ghost planes from A's K*r-deep halo)
-                if pending:
-                    self.exchanges.finish_pending()
                 if chain[0] == "lead":
                     self._launch_tb(node, plan, chain[1], key, chain[2])
                 elif chain[0] == "tc":
