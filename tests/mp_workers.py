@@ -249,3 +249,31 @@ def replay_rank(rank, world):
                 "rounds": dict(job.manager.rounds_started)}
     finally:
         job.close()
+
+
+def chain_wait_rank(rank, world):
+    """The flag operations around the est_tb launches of a 2-slab chain run
+    (device double): a chain overwrites A, so right before its launch the
+    stream must wait for the peers' PULLED of the round of A it just read."""
+    import paper_2512_19851_b200.ipc as ipc
+    from fakedev import FakeDevice
+    from paper_2512_19851_b200 import temporal
+
+    temporal.MIN_POINTS = 0
+    ipc.Device = lambda device=0: FakeDevice(device, tag=f"r{rank}")
+    prog, _ = _program("heat3d")
+    job = ipc.IpcGpuJob(rank, world)
+    try:
+        for aid in sorted(prog.shapes):
+            job.create_array(prog.shapes[aid])
+        seqs = []
+        for part in _split(prog.dag, 8):
+            job.dev.log.clear()
+            job.run(part)
+            log = [e for e in job.dev.log if e[0] in ("launch", "flag_write", "flag_wait")]
+            for k, e in enumerate(log):
+                if e[0] == "launch" and e[2] == "est_tb":
+                    seqs.append(log[k - 1][0] if k else None)
+        return seqs
+    finally:
+        job.close()

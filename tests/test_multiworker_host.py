@@ -67,3 +67,14 @@ def test_migration_keeps_tileless_workers_in_sequence(kind, world, shrink_to):
     assert len({tuple(r["seqs"]) for r in res}) == 1, [r["seqs"] for r in res]
     assert len({tuple(sorted(r["epochs"].items())) for r in res}) == 1
     assert sum(1 for r in res if not r["tiles_shrunk"]) == world - shrink_to
+
+
+def test_chain_launch_waits_for_peers_pulled():
+    """Every slab-chain launch is directly preceded by a wait on the peers'
+    PULLED flag: the chain overwrites A, and the peers must be done reading
+    the round of A it consumed (write-after-read)."""
+    from mp_workers import chain_wait_rank
+
+    res = spawn_local_job(2, chain_wait_rank, timeout=300)
+    for seqs in res:
+        assert seqs and all(s == "flag_wait" for s in seqs), seqs
