@@ -202,10 +202,14 @@ def owner_map_from_manifest(m: dict) -> dict:
     return owners
 
 
-def restore_tiles(job, manifest: dict, stats: dict | None = None) -> dict:
+def restore_tiles(job, manifest: dict, stats: dict | None = None, next_owners: dict | None = None) -> dict:
     """Install this worker's tiles from the daemons; returns {array: depth}.
     `stats` (optional) receives the split: daemon requests, tile-buffer
-    allocation, daemon-arena IPC mapping, copies + sync, frees (ms)."""
+    allocation, daemon-arena IPC mapping, copies + sync, frees (ms).
+    `next_owners` (optional): the owner map the following load-balance stage
+    moves to (an expand restores at the old owners, then migrates to
+    decomp.owner_map(new count), coordinator.py:520-528, 599-607); tiles that
+    will leave get arenas of their own so their new owner maps only them."""
     import time
 
     store, dev = job.store, job.dev
@@ -238,7 +242,8 @@ def restore_tiles(job, manifest: dict, stats: dict | None = None) -> dict:
                 raise ValueError(f"allocation {rec['alloc_id']} size mismatch")
             tile = store.tiles.setdefault(tuple(coords), GpuTile(tuple(coords)))
             t0 = time.perf_counter()
-            buf = TileBuffer(dev, ext, depth, int(meta.get("dtype", 0)))
+            leaving = next_owners is not None and next_owners.get(tuple(coords), job.rank) != job.rank
+            buf = TileBuffer(dev, ext, depth, int(meta.get("dtype", 0)), isolated=leaving)
             t1 = time.perf_counter()
             base = arenas.get((rec["daemon"], serial))
             if base is None:

@@ -62,20 +62,29 @@ class DevicePool:
         self.arenas: list = []
         self.live: dict = {}  # ptr -> (arena, offset, reserved bytes)
 
-    def alloc(self, nbytes: int) -> int:
+    def alloc(self, nbytes: int, isolated: bool = False) -> int:
+        """`isolated`: an arena of its own, exactly this size - for a buffer
+        that another worker is about to map (a tile an expand's load-balance
+        stage will move): the peer then maps only that buffer, not the whole
+        shared arena (cudaIpcOpenMemHandle costs ~50-65 ms per GiB)."""
         from .device import COMPUTE
 
         need = -(-max(1, int(nbytes)) // ALIGN) * ALIGN
-        for arena in self.arenas:
-            off = arena.take(need)
-            if off is not None:
-                break
-        else:
-            # room for three more buffers of this size: a shrink that doubles the
-            # tiles per worker then needs no cudaMalloc and no new peer mapping
-            arena = _Arena(self.dev, max(self.grow * need, self.arena_min))
+        if isolated:
+            arena = _Arena(self.dev, need)
             self.arenas.append(arena)
             off = arena.take(need)
+        else:
+            for arena in self.arenas:
+                off = arena.take(need)
+                if off is not None:
+                    break
+            else:
+                # room for three more buffers of this size: a shrink that doubles the
+                # tiles per worker then needs no cudaMalloc and no new peer mapping
+                arena = _Arena(self.dev, max(self.grow * need, self.arena_min))
+                self.arenas.append(arena)
+                off = arena.take(need)
         ptr = arena.base + off
         self.dev.memset_zero(ptr, need, COMPUTE)
         self.dev.stream_sync(COMPUTE)
@@ -107,9 +116,9 @@ class DevicePool:
         self.live.clear()
 
 
-def device_alloc(dev, nbytes: int) -> int:
+def device_alloc(dev, nbytes: int, isolated: bool = False) -> int:
     pool = getattr(dev, "pool", None)
-    return pool.alloc(nbytes) if pool is not None else dev.alloc(nbytes)
+    return pool.alloc(nbytes, isolated) if pool is not None else dev.alloc(nbytes)
 
 
 def device_free(dev, ptr: int) -> None:

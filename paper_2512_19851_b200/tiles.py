@@ -123,7 +123,7 @@ class TileBuffer:
                  "nz", "nbytes", "owned", "serial")
     _serials = __import__("itertools").count(1)
 
-    def __init__(self, dev: Device, ext, depth, dtype: int, ptr: int | None = None):
+    def __init__(self, dev: Device, ext, depth, dtype: int, ptr: int | None = None, isolated: bool = False):
         self.dev = dev
         self.rank = len(ext)
         self.dtype = dtype
@@ -137,7 +137,7 @@ class TileBuffer:
         self.nz = self.ext[0] + 2 * dz
         self.nbytes = self.pz * self.nz * self.elem
         self.owned = ptr is None
-        self.ptr = device_alloc(dev, self.nbytes) if ptr is None else ptr
+        self.ptr = device_alloc(dev, self.nbytes, isolated) if ptr is None else ptr
         self.serial = next(TileBuffer._serials)  # identifies this allocation in peer tables
 
     @staticmethod

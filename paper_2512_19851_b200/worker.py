@@ -254,7 +254,9 @@ class GpuWorker:
         self.job = self._new_job(decomp, owner_map_from_manifest(manifest))
         t1 = time.perf_counter()
         rst: dict = {}
-        depths = restore_tiles(self.job, manifest, rst)
+        # an expand's load-balance stage follows and moves tiles to the new
+        # count's owner map; those tiles are restored into arenas of their own
+        depths = restore_tiles(self.job, manifest, rst, next_owners=decomp.owner_map(self.worker_count))
         t2 = time.perf_counter()
         self.job.executor.depths = depths
         for a, info in self.job.store.arrays.items():
