@@ -71,8 +71,12 @@ class DevicePool:
 
         need = -(-max(1, int(nbytes)) // ALIGN) * ALIGN
         if isolated:
-            arena = _Arena(self.dev, need)
-            self.arenas.append(arena)
+            # an idle arena of this size (an earlier isolated buffer that has
+            # been freed) is reused; otherwise a new one
+            arena = next((a for a in self.arenas if a.size == need and a.free == [(0, need)]), None)
+            if arena is None:
+                arena = _Arena(self.dev, need)
+                self.arenas.append(arena)
             off = arena.take(need)
         else:
             for arena in self.arenas:

@@ -78,3 +78,21 @@ def test_chain_launch_waits_for_peers_pulled():
     res = spawn_local_job(2, chain_wait_rank, timeout=300)
     for seqs in res:
         assert seqs and all(s == "flag_wait" for s in seqs), seqs
+
+
+def test_isolated_arenas_are_reused():
+    """Isolated allocations (tiles an expand's load-balance stage moves) get
+    an arena of their own; once freed, the idle arena serves the next
+    isolated request of the same size instead of a new cudaMalloc."""
+    from fakedev import FakeDevice
+    from paper_2512_19851_b200.pool import DevicePool
+
+    dev = FakeDevice()
+    pool = DevicePool(dev, arena_min=1 << 20)
+    a = pool.alloc(3 << 20, isolated=True)
+    b = pool.alloc(3 << 20, isolated=True)
+    assert len(pool.arenas) == 2 and pool.locate(a)[0] != pool.locate(b)[0]
+    pool.free(a)
+    c = pool.alloc(3 << 20, isolated=True)
+    assert len(pool.arenas) == 2 and c == a
+    assert all(ar.size == 3 << 20 for ar in pool.arenas)  # exactly the buffer: a peer maps nothing else
